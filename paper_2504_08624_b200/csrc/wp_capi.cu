@@ -1,0 +1,613 @@
+// C ABI of libwpb200.so (declarations in include/wavepipe_b200.h).
+//
+// A plan turns the reference's stage list (Chain.stages, chain.py:27-41) into
+// fused passes and precomputes, in float64 on the host, every transfer matrix
+// the chunked IIR scan needs. Executing a plan issues one kernel per pass
+// (plus a 4-byte counter memset), never allocates and never synchronizes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <unistd.h>
+
+#include "../../include/wavepipe_b200.h"
+#include "wp_internal.h"
+
+namespace wp {
+int fused_occupancy_f32(int S, bool fir, size_t smem);
+int fused_occupancy_f64(int S, bool fir, size_t smem);
+size_t fused_smem_bytes_f32(int S, int tpad);
+size_t fused_smem_bytes_f64(int S, int tpad);
+}  // namespace wp
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+std::atomic<unsigned long long> g_epoch{0};
+std::once_flag g_epoch_once;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return WP_ECUDA;
+}
+
+unsigned long long next_epoch() {
+    std::call_once(g_epoch_once, [] {
+        // random 62-bit start so stale look-back flags left in recycled device
+        // memory can never carry the current epoch
+        unsigned long long t = (unsigned long long)std::chrono::high_resolution_clock::now().time_since_epoch().count();
+        t ^= (unsigned long long)getpid() * 0x9E3779B97F4A7C15ull;
+        t ^= t >> 29;
+        t *= 0xBF58476D1CE4E5B9ull;
+        g_epoch.store((t & ((1ull << 61) - 1)) | 1ull);
+    });
+    return g_epoch.fetch_add(1) & ((1ull << 62) - 1);
+}
+
+constexpr double kF64Radius = 0.98;
+
+// ---------------------------------------------------------------- matrices
+using Mat = std::vector<double>;  // row-major D x D
+
+Mat identity(int D) {
+    Mat m(D * D, 0.0);
+    for (int i = 0; i < D; ++i) m[i * D + i] = 1.0;
+    return m;
+}
+
+Mat matmul(const Mat &a, const Mat &b, int D) {
+    Mat c(D * D, 0.0);
+    for (int i = 0; i < D; ++i)
+        for (int k = 0; k < D; ++k) {
+            const long double aik = a[i * D + k];
+            if (aik == 0.0L) continue;
+            for (int j = 0; j < D; ++j) c[i * D + j] += (double)(aik * (long double)b[k * D + j]);
+        }
+    return c;
+}
+
+Mat matpow(const Mat &m, int e, int D) {
+    Mat r = identity(D), base = m;
+    while (e > 0) {
+        if (e & 1) r = matmul(r, base, D);
+        base = matmul(base, base, D);
+        e >>= 1;
+    }
+    return r;
+}
+
+// One DF2T cascade step: state (w1_s, w2_s) per section, input u.
+void cascade_step(const std::vector<double> &sos, int S, const double *st, double u, double *out) {
+    for (int s = 0; s < S; ++s) {
+        const double b0 = sos[5 * s], b1 = sos[5 * s + 1], b2 = sos[5 * s + 2];
+        const double a1 = sos[5 * s + 3], a2 = sos[5 * s + 4];
+        const double w1 = st[2 * s], w2 = st[2 * s + 1];
+        const double y = b0 * u + w1;
+        out[2 * s] = b1 * u - a1 * y + w2;
+        out[2 * s + 1] = b2 * u - a2 * y;
+        u = y;
+    }
+}
+
+void build_tables(wp::HostTables &t, const std::vector<double> &sos, int S, int H) {
+    const int D = 2 * S;
+    t.S = S;
+    t.D = D;
+    t.sos = sos;
+    Mat A(D * D);
+    std::vector<double> B(D), e(D), o(D);
+    for (int j = 0; j < D; ++j) {
+        std::fill(e.begin(), e.end(), 0.0);
+        e[j] = 1.0;
+        cascade_step(sos, S, e.data(), 0.0, o.data());
+        for (int i = 0; i < D; ++i) A[i * D + j] = o[i];
+    }
+    std::fill(e.begin(), e.end(), 0.0);
+    cascade_step(sos, S, e.data(), 1.0, B.data());
+    const int L = wpk::L;
+    // K[n] = A^(L-1-n) B
+    t.K.assign(L * D, 0.0);
+    std::vector<double> v = B, nv(D);
+    for (int n = L - 1; n >= 0; --n) {
+        for (int i = 0; i < D; ++i) t.K[n * D + i] = v[i];
+        for (int i = 0; i < D; ++i) {
+            long double acc = 0;
+            for (int j = 0; j < D; ++j) acc += (long double)A[i * D + j] * v[j];
+            nv[i] = (double)acc;
+        }
+        v = nv;
+    }
+    const Mat M = matpow(A, L, D);
+    t.P.assign(5 * D * D, 0.0);
+    Mat p = M;
+    for (int q = 0; q < 5; ++q) {
+        std::copy(p.begin(), p.end(), t.P.begin() + q * D * D);
+        p = matmul(p, p, D);
+    }
+    std::vector<Mat> G(33);
+    G[0] = identity(D);
+    for (int l = 1; l <= 32; ++l) G[l] = matmul(G[l - 1], M, D);
+    t.G.assign(D * D * 33, 0.0);
+    for (int l = 0; l <= 32; ++l)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) t.G[(i * D + j) * 33 + l] = G[l][i * D + j];
+    t.W.assign(wpk::NW * D * D, 0.0);
+    Mat w = identity(D);
+    for (int q = 0; q < wpk::NW; ++q) {
+        std::copy(w.begin(), w.end(), t.W.begin() + q * D * D);
+        w = matmul(w, G[32], D);
+    }
+    const int chunks = wpk::NT - H / L;
+    const Mat MT = matpow(M, chunks, D);
+    t.MT = MT;
+    t.TP.assign(33 * D * D, 0.0);
+    Mat tp = identity(D);
+    for (int j = 0; j <= 32; ++j) {
+        std::copy(tp.begin(), tp.end(), t.TP.begin() + j * D * D);
+        tp = matmul(tp, MT, D);
+    }
+}
+
+double section_radius(const double *r) {
+    const double a1 = r[3], a2 = r[4];
+    const double disc = a1 * a1 - 4.0 * a2;
+    if (disc < 0) return std::sqrt(a2);
+    const double q = std::sqrt(disc);
+    return 0.5 * std::max(std::fabs(-a1 + q), std::fabs(-a1 - q));
+}
+
+struct Pass {
+    enum Kind { FUSED = 0, NORMALIZE = 1 } kind = FUSED;
+    int S = 0;
+    std::vector<double> sos;
+    int prec_flag = 0;  // OR of stage precision flags
+    bool f64 = false;
+    int T = 0, Tpad = 0, H = 0, Lout = wpk::REGION;
+    std::vector<double> taps;
+    float pre = 1.f;
+    std::vector<float> post;
+    double target = 1.0;
+    wp::HostTables tables;
+    void *d_G = nullptr, *d_TP = nullptr;
+    float *d_taps = nullptr;
+    size_t smem = 0;
+    int grid_cap = 0;
+    std::string desc;
+    bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
+};
+
+}  // namespace
+
+struct wp_plan {
+    std::vector<Pass> passes;
+    int device = 0;
+};
+
+namespace wp {
+
+void count_launch(int n) { g_launches.fetch_add((unsigned long long)n); }
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 1;
+    }
+    return cached[dev];
+}
+
+}  // namespace wp
+
+namespace {
+
+int finalize_pass(Pass &p) {
+    if (p.kind != Pass::FUSED) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "normalize(peak=%g): peak_abs + scale", p.target);
+        p.desc = buf;
+        return WP_OK;
+    }
+    if (p.T > 0) {
+        p.Tpad = (p.T + 7) / 8 * 8;
+        p.H = (p.Tpad + wpk::L - 1) / wpk::L * wpk::L;
+        if (p.H > wpk::REGION - 8 * wpk::L) return fail(WP_EUNSUP, "FIR too long for the direct fused kernel");
+        p.Lout = wpk::REGION - p.H;
+    }
+    if (p.S > 0) {
+        double rmax = 0;
+        for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
+        if (p.prec_flag & WP_IIR_PREC_F64)
+            p.f64 = true;
+        else if (p.prec_flag & WP_IIR_PREC_F32)
+            p.f64 = false;
+        else
+            p.f64 = rmax > kF64Radius;
+        build_tables(p.tables, p.sos, p.S, p.H);
+        const size_t es = p.f64 ? sizeof(double) : sizeof(float);
+        const int D = 2 * p.S;
+        std::vector<unsigned char> gbuf(es * D * D * 33), tbuf(es * 33 * D * D);
+        for (size_t i = 0; i < p.tables.G.size(); ++i) {
+            if (p.f64)
+                reinterpret_cast<double *>(gbuf.data())[i] = p.tables.G[i];
+            else
+                reinterpret_cast<float *>(gbuf.data())[i] = (float)p.tables.G[i];
+        }
+        for (size_t i = 0; i < p.tables.TP.size(); ++i) {
+            if (p.f64)
+                reinterpret_cast<double *>(tbuf.data())[i] = p.tables.TP[i];
+            else
+                reinterpret_cast<float *>(tbuf.data())[i] = (float)p.tables.TP[i];
+        }
+        cudaError_t e = cudaMalloc(&p.d_G, gbuf.size());
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(G)");
+        e = cudaMalloc(&p.d_TP, tbuf.size());
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(TP)");
+        e = cudaMemcpy(p.d_G, gbuf.data(), gbuf.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(G)");
+        e = cudaMemcpy(p.d_TP, tbuf.data(), tbuf.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(TP)");
+    }
+    if (p.T > 0) {
+        std::vector<float> tp(p.Tpad, 0.f);
+        for (int i = 0; i < p.T; ++i) tp[i] = (float)p.taps[i];
+        cudaError_t e = cudaMalloc(&p.d_taps, sizeof(float) * p.Tpad);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(taps)");
+        e = cudaMemcpy(p.d_taps, tp.data(), sizeof(float) * p.Tpad, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(taps)");
+    }
+    p.smem = p.f64 ? wp::fused_smem_bytes_f64(p.S, p.Tpad) : wp::fused_smem_bytes_f32(p.S, p.Tpad);
+    const int occ = p.f64 ? wp::fused_occupancy_f64(p.S, p.T > 0, p.smem) : wp::fused_occupancy_f32(p.S, p.T > 0, p.smem);
+    if (occ <= 0) return fail(WP_ECUDA, "fused kernel cannot be resident (occupancy 0): " + std::string(cudaGetErrorString(cudaGetLastError())));
+    p.grid_cap = occ * wp::sm_count();
+    char buf[256];
+    snprintf(buf, sizeof buf, "fused[pre=%g iir=%d%s fir=%d post=%zu] tile=%d halo=%d smem=%zu occ=%d", (double)p.pre, p.S,
+             p.S ? (p.f64 ? "(f64)" : "(f32)") : "", p.T, p.post.size(), p.Lout, p.H, p.smem, occ);
+    p.desc = buf;
+    return WP_OK;
+}
+
+void free_pass(Pass &p) {
+    if (p.d_G) cudaFree(p.d_G);
+    if (p.d_TP) cudaFree(p.d_TP);
+    if (p.d_taps) cudaFree(p.d_taps);
+    p.d_G = p.d_TP = nullptr;
+    p.d_taps = nullptr;
+}
+
+size_t rec_bytes(const Pass &p) {
+    if (p.kind != Pass::FUSED || p.S == 0) return 0;
+    const size_t es = p.f64 ? 8 : 4;
+    return (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
+}
+
+long long tiles_per_channel(const Pass &p, long long N) { return (N + p.Lout - 1) / p.Lout; }
+
+int arch_ok() {
+    static int cached = -99;
+    if (cached == -99) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+        cudaDeviceProp prop;
+        e = cudaGetDeviceProperties(&prop, dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+        if (prop.major != 10 || prop.minor != 0) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "device %s is sm_%d%d; this build carries sm_100a code only", prop.name,
+                     prop.major, prop.minor);
+            g_err = buf;
+            cached = WP_EARCH;
+        } else {
+            cached = WP_OK;
+        }
+    }
+    return cached;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *wp_last_error(void) { return g_err.c_str(); }
+int wp_abi_version(void) { return 1; }
+uint64_t wp_launch_count(void) { return (uint64_t)g_launches.load(); }
+int wp_check_device(void) { return arch_ok(); }
+
+int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan) {
+    if (!out_plan) return fail(WP_EINVAL, "out_plan is NULL");
+    *out_plan = nullptr;
+    if (n_stages < 0 || (n_stages > 0 && !stages)) return fail(WP_EINVAL, "bad stage array");
+    int rc = arch_ok();
+    if (rc != WP_OK) return rc;
+    wp_plan *plan = new wp_plan();
+    cudaGetDevice(&plan->device);
+    std::vector<Pass> &passes = plan->passes;
+    Pass cur;
+    auto close = [&]() {
+        if (!cur.empty()) passes.push_back(cur);
+        cur = Pass();
+    };
+    for (int si = 0; si < n_stages; ++si) {
+        const wp_stage &st = stages[si];
+        switch (st.kind) {
+            case WP_STAGE_GAIN: {
+                if (!std::isfinite(st.value)) {
+                    delete plan;
+                    return fail(WP_EINVAL, "gain must be finite");
+                }
+                if (cur.S == 0 && cur.T == 0 && cur.post.empty()) {
+                    cur.pre = cur.pre * (float)st.value;
+                } else {
+                    if ((int)cur.post.size() == wpk::MAXPOST) {
+                        close();
+                        cur.pre = (float)st.value;
+                    } else {
+                        cur.post.push_back((float)st.value);
+                    }
+                }
+                break;
+            }
+            case WP_STAGE_IIR: {
+                if (st.n < 1 || !st.coef) {
+                    delete plan;
+                    return fail(WP_EINVAL, "IIR stage needs >= 1 section");
+                }
+                if (cur.T > 0 || !cur.post.empty()) close();
+                int idx = 0;
+                while (idx < st.n) {
+                    int room = wpk::MAXS - cur.S;
+                    if (room == 0) {
+                        close();
+                        room = wpk::MAXS;
+                    }
+                    const int take = std::min(room, st.n - idx);
+                    for (int s = 0; s < take; ++s)
+                        for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * (idx + s) + j]);
+                    cur.S += take;
+                    cur.prec_flag |= st.flags & (WP_IIR_PREC_F32 | WP_IIR_PREC_F64);
+                    idx += take;
+                }
+                break;
+            }
+            case WP_STAGE_FIR: {
+                if (st.n < 1 || !st.coef) {
+                    delete plan;
+                    return fail(WP_EINVAL, "FIR stage needs >= 1 tap");
+                }
+                if (cur.T > 0 || !cur.post.empty()) close();
+                cur.T = st.n;
+                cur.taps.assign(st.coef, st.coef + st.n);
+                break;
+            }
+            case WP_STAGE_NORMALIZE: {
+                if (!(st.value > 0) || !std::isfinite(st.value)) {
+                    delete plan;
+                    return fail(WP_EINVAL, "normalize target must be finite and > 0");
+                }
+                close();
+                Pass n;
+                n.kind = Pass::NORMALIZE;
+                n.target = st.value;
+                passes.push_back(n);
+                break;
+            }
+            default:
+                delete plan;
+                return fail(WP_EINVAL, "unknown stage kind " + std::to_string(st.kind));
+        }
+    }
+    close();
+    if (passes.empty()) passes.push_back(Pass());  // identity copy
+    for (Pass &p : passes) {
+        rc = finalize_pass(p);
+        if (rc != WP_OK) {
+            for (Pass &q : passes) free_pass(q);
+            delete plan;
+            return rc;
+        }
+    }
+    *out_plan = plan;
+    return WP_OK;
+}
+
+int wp_plan_destroy(wp_plan *plan) {
+    if (!plan) return WP_OK;
+    for (Pass &p : plan->passes) free_pass(p);
+    delete plan;
+    return WP_OK;
+}
+
+int wp_plan_num_passes(const wp_plan *plan) { return plan ? (int)plan->passes.size() : 0; }
+
+int wp_plan_launches(const wp_plan *plan) {
+    if (!plan) return 0;
+    int n = 0;
+    for (const Pass &p : plan->passes) n += p.kind == Pass::FUSED ? 1 : 2;
+    return n;
+}
+
+const char *wp_plan_describe(const wp_plan *plan, int32_t pass) {
+    if (!plan || pass < 0 || pass >= (int)plan->passes.size()) return "";
+    return plan->passes[pass].desc.c_str();
+}
+
+static size_t ws_layout(const wp_plan *plan, int64_t C, int64_t N, size_t *rec_off, size_t *tmp_off, int64_t *ld_tmp) {
+    size_t recb = 0;
+    for (const Pass &p : plan->passes) recb = std::max(recb, rec_bytes(p) * (size_t)(tiles_per_channel(p, N) * C));
+    *rec_off = 256;
+    *tmp_off = (256 + recb + 255) / 256 * 256;
+    *ld_tmp = (N + 63) / 64 * 64;
+    const size_t tmpb = plan->passes.size() >= 2 ? sizeof(float) * (size_t)C * (size_t)(*ld_tmp) : 0;
+    return *tmp_off + tmpb;
+}
+
+int wp_plan_workspace_bytes(const wp_plan *plan, int64_t channels, int64_t frames, size_t *bytes) {
+    if (!plan || !bytes) return fail(WP_EINVAL, "null argument");
+    if (channels < 1 || frames < 1) return fail(WP_EINVAL, "need channels >= 1 and frames >= 1");
+    size_t a, b;
+    int64_t ld;
+    *bytes = ws_layout(plan, channels, frames, &a, &b, &ld);
+    return WP_OK;
+}
+
+int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, int64_t N, int64_t ldx, int64_t ldy,
+                    void *workspace, size_t workspace_bytes, wp_stream_t stream_) {
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+    if (!plan) return fail(WP_EINVAL, "plan is NULL");
+    if (!x || !y) return fail(WP_EINVAL, "x and y must be device pointers");
+    if (C < 1 || N < 1) return fail(WP_EINVAL, "need channels >= 1 and frames >= 1");
+    if (ldx < N || ldy < N) return fail(WP_EINVAL, "row stride smaller than frames");
+    {
+        const char *xb = reinterpret_cast<const char *>(x), *xe = xb + sizeof(float) * ((C - 1) * ldx + N);
+        const char *yb = reinterpret_cast<const char *>(y), *ye = yb + sizeof(float) * ((C - 1) * ldy + N);
+        if (xb < ye && yb < xe) return fail(WP_EINVAL, "x and y overlap");
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != plan->device) return fail(WP_EINVAL, "plan was created on another device");
+    size_t rec_off, tmp_off;
+    int64_t ld_tmp;
+    const size_t need = ws_layout(plan, C, N, &rec_off, &tmp_off, &ld_tmp);
+    if (!workspace || workspace_bytes < need)
+        return fail(WP_ENOMEM, "workspace too small: need " + std::to_string(need) + " bytes");
+    unsigned char *ws = reinterpret_cast<unsigned char *>(workspace);
+    unsigned int *counter = reinterpret_cast<unsigned int *>(ws);
+    unsigned int *peak = reinterpret_cast<unsigned int *>(ws + 64);
+    float *tmp = reinterpret_cast<float *>(ws + tmp_off);
+    const int P = (int)plan->passes.size();
+    const float *in = x;
+    int64_t ld_in = ldx;
+    for (int i = 0; i < P; ++i) {
+        const Pass &p = plan->passes[i];
+        const bool to_y = ((P - 1 - i) % 2) == 0;
+        float *out = to_y ? y : tmp;
+        const int64_t ld_out = to_y ? ldy : ld_tmp;
+        cudaError_t e;
+        if (p.kind == Pass::NORMALIZE) {
+            e = cudaMemsetAsync(peak, 0, sizeof(unsigned int), stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset(peak)");
+            e = wp::launch_peak_abs(in, C, N, ld_in, peak, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "peak_abs launch");
+            e = wp::launch_scale_by_peak(in, out, C, N, ld_in, ld_out, peak, (float)p.target, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "scale launch");
+        } else {
+            wpk::FusedArgs a{};
+            a.x = in;
+            a.y = out;
+            a.C = C;
+            a.N = N;
+            a.ldx = ld_in;
+            a.ldy = ld_out;
+            a.Lout = p.Lout;
+            a.H = p.H;
+            a.Tpad = p.Tpad;
+            a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+            a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+            a.taps = p.d_taps;
+            a.pre_gain = p.pre;
+            a.n_post = (int)p.post.size();
+            for (int j = 0; j < a.n_post; ++j) a.post[j] = p.post[j];
+            a.G = p.d_G;
+            a.TP = p.d_TP;
+            a.counter = counter;
+            a.recs = ws + rec_off;
+            a.epoch = next_epoch();
+            const long long tpc = tiles_per_channel(p, N);
+            a.total_tiles = tpc * C;
+            const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
+            e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset(counter)");
+            e = p.f64 ? wp::launch_fused_f64(p.S, p.T > 0, a, p.tables, grid, p.smem, stream)
+                      : wp::launch_fused_f32(p.S, p.T > 0, a, p.tables, grid, p.smem, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
+        }
+        in = out;
+        ld_in = ld_out;
+    }
+    return WP_OK;
+}
+
+// ---- seam-level one-shot entry points with a small plan cache ----
+static std::mutex g_cache_mu;
+static std::map<std::string, wp_plan *> g_cache;
+
+static int cached_plan(const wp_stage &st, wp_plan **out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::string key((const char *)&st.kind, sizeof st.kind);
+    key.append((const char *)&st.flags, sizeof st.flags);
+    key.append((const char *)&dev, sizeof dev);
+    key.append((const char *)st.coef, sizeof(double) * (size_t)st.n * (st.kind == WP_STAGE_IIR ? 5 : 1));
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+        *out = it->second;
+        return WP_OK;
+    }
+    if (g_cache.size() >= 64) {
+        // rare path: drop everything (cudaFree synchronizes the device)
+        for (auto &kv : g_cache) wp_plan_destroy(kv.second);
+        g_cache.clear();
+    }
+    int rc = wp_plan_create(&st, 1, out);
+    if (rc == WP_OK) g_cache[key] = *out;
+    return rc;
+}
+
+int wp_iir_cascade(const double *sos, int32_t n_sections, const float *x, float *y, int64_t channels, int64_t frames,
+                   int64_t ld_x, int64_t ld_y, int32_t flags, void *workspace, size_t workspace_bytes,
+                   wp_stream_t stream) {
+    wp_stage st{WP_STAGE_IIR, n_sections, sos, 0.0, flags, 0};
+    if (n_sections < 1 || !sos) return fail(WP_EINVAL, "need >= 1 section");
+    wp_plan *plan = nullptr;
+    int rc = cached_plan(st, &plan);
+    if (rc != WP_OK) return rc;
+    return wp_plan_execute(plan, x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+}
+
+int wp_fir(const double *taps, int32_t n_taps, const float *x, float *y, int64_t channels, int64_t frames, int64_t ld_x,
+           int64_t ld_y, int32_t flags, void *workspace, size_t workspace_bytes, wp_stream_t stream) {
+    wp_stage st{WP_STAGE_FIR, n_taps, taps, 0.0, flags, 0};
+    if (n_taps < 1 || !taps) return fail(WP_EINVAL, "need >= 1 tap");
+    wp_plan *plan = nullptr;
+    int rc = cached_plan(st, &plan);
+    if (rc != WP_OK) return rc;
+    return wp_plan_execute(plan, x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+}
+
+int wp_white_noise(float *y, int64_t channels, int64_t frames, int64_t ld_y, uint64_t seed, wp_stream_t stream) {
+    if (!y || channels < 1 || frames < 1 || ld_y < frames) return fail(WP_EINVAL, "bad noise arguments");
+    int rc = arch_ok();
+    if (rc != WP_OK) return rc;
+    cudaError_t e = wp::launch_white_noise(y, channels, frames, ld_y, seed, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? WP_OK : cuda_fail(e, "white_noise launch");
+}
+
+int wp_peak_abs(const float *x, int64_t channels, int64_t frames, int64_t ld_x, float *out_device, wp_stream_t stream) {
+    if (!x || !out_device || channels < 1 || frames < 1 || ld_x < frames) return fail(WP_EINVAL, "bad peak arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(out_device, 0, sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset(peak)");
+    e = wp::launch_peak_abs(x, channels, frames, ld_x, reinterpret_cast<unsigned int *>(out_device), s);
+    return e == cudaSuccess ? WP_OK : cuda_fail(e, "peak launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// Internal host-side interfaces shared by the C-ABI translation unit and the
+// per-dtype kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "wp_fused.cuh"
+
+namespace wp {
+
+// float64 scan tables of one fused IIR block (D = 2S), computed on the host.
+struct HostTables {
+    int S = 0;
+    int D = 1;
+    std::vector<double> sos;  // [S][5]
+    std::vector<double> K;    // [L][D]
+    std::vector<double> P;    // [5][D][D]
+    std::vector<double> W;    // [NW][D][D]
+    std::vector<double> MT;   // [D][D]
+    std::vector<double> G;    // [D][D][33]  lane-minor
+    std::vector<double> TP;   // [33][D][D]
+};
+
+// Launch one fused pass. `grid` = number of persistent CTAs.
+cudaError_t launch_fused_f32(int S, bool fir, const wpk::FusedArgs &a, const HostTables &t, int grid,
+                             size_t smem, cudaStream_t st);
+cudaError_t launch_fused_f64(int S, bool fir, const wpk::FusedArgs &a, const HostTables &t, int grid,
+                             size_t smem, cudaStream_t st);
+// Max resident CTAs per SM for the instantiation (0 on error).
+int fused_occupancy(bool f64, int S, bool fir, size_t smem);
+size_t fused_smem_bytes(bool f64, int S, int tpad);
+
+// misc kernels (wp_misc.cu)
+cudaError_t launch_white_noise(float *y, long long C, long long N, long long ld, unsigned long long seed,
+                               cudaStream_t st);
+cudaError_t launch_peak_abs(const float *x, long long C, long long N, long long ld, unsigned int *out_bits,
+                            cudaStream_t st);
+cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long long N, long long ldx, long long ldy,
+                                 const unsigned int *peak_bits, float target, cudaStream_t st);
+
+void count_launch(int n = 1);
+int sm_count();
+
+}  // namespace wp

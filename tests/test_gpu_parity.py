@@ -1,0 +1,289 @@
+"""GPU parity: the sm_100a path (through the public API -> C ABI) against the
+reference's own outputs (golden fixtures) and the CPU oracle.
+
+Bars (SURVEY.md §8c / BASELINE.md §4), metric max|y - y_ref| / max|y_ref|:
+FIR <= 1e-5, IIR cascades and chains <= 1e-4 (the scan re-associates the
+recurrence into 64-sample chunks; IIR blocks with pole radius > 0.98 run in
+float64). Known-answer tests of the reference are exact.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2504_08624_b200 as wp
+from paper_2504_08624_b200 import _native
+
+from conftest import iir_from_entry, random_cascade, random_unbound_stage
+
+pytestmark = pytest.mark.gpu
+
+FIR_TOL = 1e-5
+IIR_TOL = 1e-4
+
+
+def _cfg3():
+    return [
+        wp.design_butterworth("hp", 4, 100),
+        wp.design_chebyshev1("lp", 4, 1.0, 8000),
+        wp.design_fir("lp", 101, 15000),
+        wp.Gain(0.5),
+    ]
+
+
+def _bench_chain():
+    return [
+        wp.design_butterworth("lowpass", 4, 1000.0),
+        wp.design_butterworth("lowpass", 4, 1200.0),
+        wp.design_chebyshev1("lowpass", 4, 1.0, 2000.0),
+        wp.design_chebyshev1("lowpass", 4, 1.0, 2400.0),
+    ]
+
+
+GOLDEN_CASES = {
+    "cfg1": (44100, lambda D: [wp.design_butterworth("lp", 4, 1000)], IIR_TOL),
+    "cfg2": (48000, lambda D: [wp.design_fir("lp", 101, 1000, "hamming")], FIR_TOL),
+    "cfg3_noise": (48000, lambda D: _cfg3(), IIR_TOL),
+    "cfg3_sine": (48000, lambda D: _cfg3(), IIR_TOL),
+    "cfg4": (48000, lambda D: [wp.design_fir("lp", 4096, 2000, "hamming")], FIR_TOL),
+    "cfg5": (48000, lambda D: [wp.design_butterworth("lp", 8, 2000)], IIR_TOL),
+    "bench_chain": (44100, lambda D: _bench_chain(), IIR_TOL),
+    "mixed_fir_peak": (44100, lambda D: [wp.design_fir("lowpass", 33, 4000), wp.design_peaking(1000, gain_db=2.0)], IIR_TOL),
+    "shelves": (44100, lambda D: [wp.design_shelf("hi_shelf", 1000, gain_db=3.0), wp.design_shelf("lo_shelf", 2000, gain_db=3.0)], IIR_TOL),
+}
+for _i in range(6):
+    GOLDEN_CASES[f"random_cascade_{_i}"] = (44100, (lambda i: lambda D: [iir_from_entry(D[f"random_cascade_{i}"], 44100)])(_i), IIR_TOL)
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN_CASES))
+def test_golden_reference_outputs(name, golden_vectors, golden_designs):
+    """Reference (wavepipe, float64) output on the same fp32-rounded input."""
+    fs, build, tol = GOLDEN_CASES[name]
+    x = golden_vectors[f"{name}__x"]
+    y_ref = golden_vectors[f"{name}__y"]
+    w = wp.Wave(x, fs)
+    y = wp.pipe(w, wp.Chain(build(golden_designs)))
+    err = oracle.parity_error(y.samples, y_ref)
+    assert err <= tol, f"{name}: parity {err:.3e} > {tol:g}"
+
+
+@pytest.mark.parametrize("i", range(4))
+@pytest.mark.parametrize("strategy", ["direct", "fft"])
+def test_golden_random_fir(i, strategy, golden_vectors, golden_designs):
+    taps = golden_designs[f"random_fir_{i}"]["taps"]
+    x = golden_vectors[f"random_fir_{i}_{strategy}__x"]
+    y_ref = golden_vectors[f"random_fir_{i}_{strategy}__y"]
+    filt = wp.FirFilter.from_taps(taps, fs=44100)
+    y = wp.apply_fir(filt, wp.Wave(x, 44100), strategy=strategy)
+    assert oracle.parity_error(y.samples, y_ref) <= FIR_TOL
+
+
+# ---- known-answer tests of the reference (test_engine.py) -------------------
+
+
+def test_iir_identity_bit_exact(rng):
+    w = wp.Wave(rng.standard_normal((3, 1000)), 44100)
+    ident = wp.IirFilter.from_sections([wp.BiquadSection(1.0, 0.0, 0.0, 0.0, 0.0)], fs=44100)
+    assert np.array_equal(wp.apply_iir(ident, w).samples, w.samples)
+
+
+def test_one_pole_impulse_exact():
+    impulse = np.zeros(8)
+    impulse[0] = 1.0
+    one_pole = wp.IirFilter.from_sections([wp.BiquadSection(1.0, 0.0, 0.0, -0.5, 0.0)], fs=44100)
+    out = wp.apply_iir(one_pole, wp.Wave([impulse], 44100))
+    np.testing.assert_array_equal(out.samples[0], 0.5 ** np.arange(8))
+
+
+def test_one_pole_long_impulse_crosses_tiles():
+    n = 50000  # spans several tiles, exercises the look-back
+    x = np.zeros(n)
+    x[0] = 1.0
+    f = wp.IirFilter.from_sections([wp.BiquadSection(1.0, 0.0, 0.0, -0.9995, 0.0)], fs=44100)
+    out = wp.apply_iir(f, wp.Wave([x], 44100)).samples[0]
+    expect = 0.9995 ** np.arange(n)
+    assert np.max(np.abs(out - expect)) <= 1e-4
+
+
+@pytest.mark.parametrize(
+    "taps,x,expect",
+    [
+        ([1.0], None, None),
+        ([0.0, 1.0], [1.0, 2.0, 3.0], [0.0, 1.0, 2.0]),
+        ([0.5, 0.5], [1.0, 0.0, 0.0, 0.0], [0.5, 0.5, 0.0, 0.0]),
+        ([0.25, 0.25, 0.25, 0.25], [1.0, 1.0], [0.25, 0.5]),
+    ],
+)
+def test_fir_known_answers(taps, x, expect, rng):
+    if x is None:
+        w = wp.Wave(rng.standard_normal((2, 1000)), 44100)
+        out = wp.apply_fir(wp.FirFilter.from_taps(taps, fs=44100), w, strategy="direct")
+        assert np.array_equal(out.samples, w.samples)
+    else:
+        out = wp.apply_fir(wp.FirFilter.from_taps(taps, fs=44100), wp.Wave([x], 44100), strategy="direct")
+        np.testing.assert_array_equal(out.samples[0], expect)
+
+
+def test_fir_fft_tiny_signal():
+    w = wp.Wave([[1.0, 2.0]], 44100)
+    f = wp.FirFilter.from_taps([0.5, 0.25, 0.125], fs=44100)
+    d = wp.apply_fir(f, w, strategy="direct").samples
+    ff = wp.apply_fir(f, w, strategy="fft").samples
+    np.testing.assert_allclose(ff, d, atol=1e-6)
+
+
+# ---- oracle parity on fresh seeded inputs ---------------------------------
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_cascades_vs_oracle(seed):
+    rng = np.random.default_rng(0xACCE01 + seed)
+    filt = random_cascade(rng, max_sections=6)
+    frames = int(10 ** rng.uniform(3, 5))
+    channels = int(rng.integers(1, 13))
+    w = wp.Wave(rng.standard_normal((channels, frames)), 44100)
+    y = wp.apply_iir(filt, w).samples
+    ref = oracle.iir_cascade(filt.sos_rows(), w.samples)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_forced_precision_paths(precision):
+    rng = np.random.default_rng(7)
+    filt = wp.design_butterworth("lp", 8, 2000, 48000)
+    w = wp.Wave(rng.standard_normal((3, 70000)), 48000)
+    wp.set_iir_precision(precision)
+    try:
+        y = wp.apply_iir(filt, w).samples
+    finally:
+        wp.set_iir_precision("auto")
+    assert oracle.parity_error(y, oracle.iir_cascade(filt.sos_rows(), w.samples)) <= IIR_TOL
+
+
+@pytest.mark.parametrize("n_taps", [3, 31, 101, 257, 1025])
+def test_fir_direct_vs_oracle(n_taps):
+    rng = np.random.default_rng(n_taps)
+    taps = rng.standard_normal(n_taps) / np.sqrt(n_taps)
+    w = wp.Wave(rng.standard_normal((3, 40000 + n_taps)), 44100)
+    y = wp.apply_fir(wp.FirFilter.from_taps(taps, 44100), w, strategy="direct").samples
+    assert oracle.parity_error(y, oracle.fir_direct(taps, w.samples)) <= FIR_TOL
+
+
+def test_ragged_shapes_and_unaligned_rows():
+    rng = np.random.default_rng(3)
+    chain = [wp.design_butterworth("hp", 2, 300, 44100), wp.design_fir("lp", 17, 5000, fs=44100), wp.Gain(2.0)]
+    for frames in (1, 2, 3, 5, 63, 64, 65, 8063, 8064, 8065, 8191, 8192, 8193, 20001):
+        w = wp.Wave(rng.standard_normal((2, frames)), 44100)
+        y = wp.pipe(w, wp.Chain(chain)).samples
+        ref = oracle.pipe(w.samples, chain)
+        assert oracle.parity_error(y, ref) <= IIR_TOL, frames
+
+
+def test_normalize_stage():
+    rng = np.random.default_rng(5)
+    w = wp.Wave(rng.standard_normal((4, 5000)) * 3.0, 44100)
+    y = (w | wp.design_butterworth("lp", 2, 1000) | wp.Normalize(0.5)).samples
+    ref = oracle.pipe(w.samples, [wp.design_butterworth("lp", 2, 1000, 44100), wp.Normalize(0.5)])
+    assert oracle.parity_error(y, ref) <= IIR_TOL
+    assert abs(np.max(np.abs(y)) - 0.5) < 1e-6
+
+
+# ---- determinism and algebra (bit-exact) -----------------------------------
+
+
+def test_channel_independence_bit_exact():
+    rng = np.random.default_rng(11)
+    filt = random_cascade(rng)
+    w = wp.Wave(rng.standard_normal((4, 30000)), 44100)
+    full = wp.apply_iir(filt, w)
+    for c in range(4):
+        assert np.array_equal(full.samples[c], wp.apply_iir(filt, w.channel(c)).samples[0])
+
+
+def test_repeat_runs_bit_identical():
+    w = wp.white_noise(3.0, 8, 48000, seed=9)
+    chain = wp.Chain(_cfg3())
+    a = wp.pipe(w, chain).samples
+    for _ in range(3):
+        assert np.array_equal(wp.pipe(w, chain).samples, a)
+
+
+def test_pipe_compose_coherence_bit_exact():
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        w = wp.Wave(rng.standard_normal((2, 257)), 44100)
+        left = wp.Chain([random_unbound_stage(rng) for _ in range(int(rng.integers(0, 3)))])
+        right = wp.Chain([random_unbound_stage(rng) for _ in range(int(rng.integers(1, 3)))])
+        composed = wp.compose(left, right)
+        assert wp.pipe(wp.pipe(w, left), right) == wp.pipe(w, composed)
+        assert wp.pipe(w, composed) == wp.pipe(w, composed.bind(w.fs))
+
+
+def test_wave_or_operator_and_custom_stage():
+    w = wp.white_noise(0.05, 2, 44100, seed=11)
+    hi, lo = wp.design_shelf("hi_shelf", 1000, gain_db=3.0), wp.design_shelf("lo_shelf", 2000, gain_db=3.0)
+    assert (w | hi | lo) == wp.pipe(wp.pipe(w, hi), lo)
+
+    class Half:
+        def bind(self, fs):
+            return self
+
+        def apply(self, wave, backend="auto"):
+            return wp.Wave(wave.samples * 0.5, fs=wave.fs)
+
+    out = wp.pipe(w, wp.compose(Half(), wp.design_peaking(1000, gain_db=0.0)))
+    np.testing.assert_array_equal(out.samples, w.samples * 0.5)
+
+
+# ---- device noise generator ---------------------------------------------------
+
+
+def test_white_noise_matches_reference_stream(golden_noise):
+    w = wp.white_noise(5, 1, 8000, seed=7)
+    head = np.array(golden_noise["seed7_head"])
+    np.testing.assert_allclose(w.samples[0, :5], head, rtol=0, atol=1e-6)
+    multi = wp.white_noise(0.01, 3, 48000, seed=42).samples
+    ref = np.array(golden_noise["seed42_3ch_480"]).astype(np.float32).astype(np.float64)
+    assert np.max(np.abs(multi - ref)) <= 1e-6
+
+
+def test_white_noise_large_prefix_stable():
+    a = wp.white_noise(2.0, 1, 48000, seed=3).samples
+    b = wp.white_noise(2.0, 4, 48000, seed=3).samples
+    assert np.array_equal(a[0], b[0])
+    ref = oracle.white_noise(2.0, 4, 48000, 3).astype(np.float32).astype(np.float64)
+    assert np.max(np.abs(b - ref)) <= 1e-6
+
+
+# ---- full-size properties (BASELINE configs) -------------------------------
+
+
+def test_cfg3_full_size_prefix_parity():
+    """cfg3 at full size (32 x 5.76 M); the oracle checks a 4-channel, 1 s
+    prefix (all filters are causal: the output prefix depends only on the
+    input prefix)."""
+    fs = 48000
+    w = wp.white_noise(120.0, 32, fs, seed=42)
+    y = wp.pipe(w, wp.Chain(_cfg3()))
+    t = y.tensor()
+    assert t.shape == (32, 5_760_000)
+    sub = [0, 13, 31]
+    x = w.tensor()[sub, :48000].cpu().numpy().astype(np.float64)
+    ref = oracle.pipe(x, wp.Chain(_cfg3()).bind(fs).stages)
+    got = t[sub, :48000].cpu().numpy().astype(np.float64)
+    assert oracle.parity_error(got, ref) <= IIR_TOL
+    # linearity across the whole buffer: chain(2x) == 2 chain(x) within fp32 rounding
+    import torch
+
+    y2 = wp.pipe(wp.Wave.from_tensor(w.tensor() * 2.0, fs), wp.Chain(_cfg3())).tensor()
+    rel = (torch.max(torch.abs(y2 - 2.0 * t)) / torch.max(torch.abs(2.0 * t))).item()
+    assert rel <= 1e-4
+
+
+def test_plan_launch_accounting():
+    plan = _native.Plan(tuple(wp.engine._entry(s) for s in wp.Chain(_cfg3()).bind(48000).stages))
+    assert plan.num_passes == 1  # IIR(4 sections) -> FIR -> gain fused into one pass
+    assert plan.launches == 1
+    before = _native.launch_count()
+    wp.pipe(wp.white_noise(1.0, 2, 48000, seed=1), wp.Chain(_cfg3())).tensor()
+    assert _native.launch_count() - before == 2  # noise + one fused chain kernel
