@@ -4,6 +4,7 @@
 // fused passes and precomputes, in float64 on the host, every transfer matrix
 // the chunked IIR scan needs. Executing a plan issues one kernel per pass
 // (plus a 4-byte counter memset), never allocates and never synchronizes.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <cstdlib>
 #include <unistd.h>
 
 #include "../../include/wavepipe_b200.h"
@@ -186,6 +188,12 @@ struct Pass {
     float *d_taps = nullptr;
     size_t smem = 0;
     int grid_cap = 0;
+    int fir_flags = 0;
+    // tensor-core FIR (FIR-only passes)
+    bool fir_tc = false;
+    int tc_Tp = 0, tc_K = 0, tc_W = 0;
+    float tc_out_scale = 1.f;
+    unsigned char *d_Bimg = nullptr;
     std::string desc;
     bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
 };
@@ -218,10 +226,60 @@ int sm_count() {
 
 namespace {
 
+bool fir_tc_enabled() {
+    const char *v = std::getenv("WP_FIR_IMPL");
+    return !(v && std::string(v) == "cuda");
+}
+
 int finalize_pass(Pass &p) {
     if (p.kind != Pass::FUSED) {
         char buf[128];
         snprintf(buf, sizeof buf, "normalize(peak=%g): peak_abs + scale", p.target);
+        p.desc = buf;
+        return WP_OK;
+    }
+    if (p.S == 0 && p.T >= 8 && fir_tc_enabled()) {
+        // tensor-core direct FIR: rows of 64 samples, K covers taps + 63 phases
+        p.tc_Tp = (p.T - 1 + 7) / 8 * 8;
+        p.tc_K = (p.tc_Tp + wpk::TC_N + 15) / 16 * 16;
+        p.tc_W = wpk::TC_N * (wpk::TC_M - 1) + p.tc_K;
+        p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
+    }
+    if (p.fir_tc) {
+        double hmax = 0;
+        for (double v : p.taps) hmax = std::max(hmax, std::fabs(v));
+        int ex = 0;
+        if (hmax > 0) std::frexp(hmax, &ex);
+        const int f = hmax > 0 ? 14 - ex : 0;
+        p.tc_out_scale = (float)std::ldexp(1.0, -f);
+        // B image, K-major SWIZZLE_128B: [split][K atom of 64][row p][128 B],
+        // 16-byte chunks XOR-swizzled by (row & 7)
+        const int atoms = (p.tc_K + 63) / 64;
+        const size_t split = (size_t)atoms * 8192 / sizeof(__half);
+        std::vector<__half> img(2 * split, __float2half_rn(0.f));
+        for (int pcol = 0; pcol < wpk::TC_N; ++pcol)
+            for (int k = 0; k < p.tc_K; ++k) {
+                const int t = pcol + p.tc_Tp - k;
+                const float val = (t >= 0 && t < p.T) ? (float)std::ldexp(p.taps[t], f) : 0.f;
+                const __half hi = __float2half_rn(val);
+                const __half lo = __float2half_rn((val - __half2float(hi)) * 2048.f);
+                const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)pcol * 128u + (uint32_t)(k % 64) * 2u;
+                const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
+                img[phys / 2] = hi;
+                img[split + phys / 2] = lo;
+            }
+        cudaError_t e = cudaMalloc(&p.d_Bimg, img.size() * sizeof(__half));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");
+        e = cudaMemcpy(p.d_Bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(Bimg)");
+        p.smem = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K);
+        const int occ = wp::fir_tc_occupancy(p.smem);
+        if (occ <= 0) return fail(WP_ECUDA, "tensor-core FIR kernel cannot be resident");
+        p.grid_cap = occ * wp::sm_count();
+        p.Lout = wpk::TC_TOUT;
+        char buf[256];
+        snprintf(buf, sizeof buf, "fir_tc[pre=%g taps=%d K=%d post=%zu] tcgen05 f16x3 M128xN64 SW128 tile=%d smem=%zu occ=%d",
+                 (double)p.pre, p.T, p.tc_K, p.post.size(), wpk::TC_TOUT, p.smem, occ);
         p.desc = buf;
         return WP_OK;
     }
@@ -285,6 +343,8 @@ int finalize_pass(Pass &p) {
 }
 
 void free_pass(Pass &p) {
+    if (p.d_Bimg) cudaFree(p.d_Bimg);
+    p.d_Bimg = nullptr;
     if (p.d_G) cudaFree(p.d_G);
     if (p.d_TP) cudaFree(p.d_TP);
     if (p.d_taps) cudaFree(p.d_taps);
@@ -508,6 +568,31 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             if (e != cudaSuccess) return cuda_fail(e, "peak_abs launch");
             e = wp::launch_scale_by_peak(in, out, C, N, ld_in, ld_out, peak, (float)p.target, stream);
             if (e != cudaSuccess) return cuda_fail(e, "scale launch");
+        } else if (p.fir_tc) {
+            wpk::FirTcArgs a{};
+            a.x = in;
+            a.y = out;
+            a.C = C;
+            a.N = N;
+            a.ldx = ld_in;
+            a.ldy = ld_out;
+            a.total_tiles = ((N + wpk::TC_TOUT - 1) / wpk::TC_TOUT) * C;
+            a.Tp = p.tc_Tp;
+            a.K = p.tc_K;
+            a.W = p.tc_W;
+            a.Bimg = p.d_Bimg;
+            a.out_scale = p.tc_out_scale;
+            a.pre_gain = p.pre;
+            a.n_post = (int)p.post.size();
+            for (int j = 0; j < a.n_post; ++j) a.post[j] = p.post[j];
+            a.counter = counter;
+            a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+            a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+            const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
+            e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset(counter)");
+            e = wp::launch_fir_tc(a, grid, p.smem, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "fir_tc launch");
         } else {
             wpk::FusedArgs a{};
             a.x = in;

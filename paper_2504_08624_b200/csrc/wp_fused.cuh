@@ -205,15 +205,31 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
         float *yr = a.y + c * a.ldy;
 
         // ---- load region (coalesced) into the swizzled chunk layout ----
-        for (int q4 = tid; q4 < REGION / 4; q4 += NT) {
-            float4 v = load_region4(xr, r0 + 4 * q4, a.N, a.vec_x);
-            if (a.pre_gain != 1.f) {
-                v.x *= a.pre_gain;
-                v.y *= a.pre_gain;
-                v.z *= a.pre_gain;
-                v.w *= a.pre_gain;
+        {
+            constexpr int NB = 8;  // float4 loads in flight per thread
+            const bool interior = a.vec_x && r0 >= 0 && r0 + REGION <= a.N;
+#pragma unroll 1
+            for (int q0 = 0; q0 < REGION / 4; q0 += NB * NT) {
+                float4 v[NB];
+                if (interior) {
+#pragma unroll
+                    for (int j = 0; j < NB; ++j)
+                        v[j] = __ldcs(reinterpret_cast<const float4 *>(xr + r0) + q0 + tid + j * NT);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) v[j] = load_region4(xr, r0 + 4 * (q0 + tid + j * NT), a.N, a.vec_x);
+                }
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    if (a.pre_gain != 1.f) {
+                        v[j].x *= a.pre_gain;
+                        v[j].y *= a.pre_gain;
+                        v[j].z *= a.pre_gain;
+                        v[j].w *= a.pre_gain;
+                    }
+                    reg4[swz(q0 + tid + j * NT)] = v[j];
+                }
             }
-            reg4[swz(q4)] = v;
         }
         __syncthreads();
 

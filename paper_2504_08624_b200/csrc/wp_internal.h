@@ -10,6 +10,28 @@
 
 #include "wp_fused.cuh"
 
+namespace wpk {
+constexpr int TC_M = 128;                     // UMMA M: rows of the Hankel operand
+constexpr int TC_N = 64;                      // UMMA N: output phases per row (= row stride)
+constexpr int TC_TOUT = TC_M * TC_N;          // outputs per tile (8192)
+
+struct FirTcArgs {
+    const float *x;
+    float *y;
+    long long C, N, ldx, ldy;
+    long long total_tiles;
+    int Tp, K, W;
+    const unsigned char *Bimg;  // [2][K/16][512]
+    float out_scale;            // 2^-f of the taps
+    float pre_gain;
+    int n_post;
+    float post[MAXPOST];
+    unsigned int *counter;
+    int vec_x, vec_y;
+};
+
+}  // namespace wpk
+
 namespace wp {
 
 // float64 scan tables of one fused IIR block (D = 2S), computed on the host.
@@ -41,6 +63,11 @@ cudaError_t launch_peak_abs(const float *x, long long C, long long N, long long 
                             cudaStream_t st);
 cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long long N, long long ldx, long long ldy,
                                  const unsigned int *peak_bits, float target, cudaStream_t st);
+
+// tensor-core FIR (wp_fir_tc.cu)
+size_t fir_tc_smem_bytes(int W, int K);
+cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
+int fir_tc_occupancy(size_t smem);
 
 void count_launch(int n = 1);
 int sm_count();

@@ -287,3 +287,29 @@ def test_plan_launch_accounting():
     before = _native.launch_count()
     wp.pipe(wp.white_noise(1.0, 2, 48000, seed=1), wp.Chain(_cfg3())).tensor()
     assert _native.launch_count() - before == 2  # noise + one fused chain kernel
+
+
+@pytest.mark.parametrize("scale", [1e-6, 1.0, 3e4, 1e9])
+def test_fir_tensor_core_dynamic_range(scale):
+    """The tcgen05 split-fp16 FIR rescales each tile by a power of two, so the
+    result is independent of the signal's absolute magnitude."""
+    rng = np.random.default_rng(17)
+    taps = wp.design_fir("lp", 101, 1000, "hamming", 48000).taps
+    x = rng.standard_normal((3, 30000)) * scale
+    x[1, 5000:12000] = 0.0  # silent stretch inside a channel
+    w = wp.Wave(x, 48000)
+    plan = wp.engine.plan_for([wp.FirFilter.from_taps(taps, 48000)])
+    assert "fir_tc" in plan.describe()[0]
+    y = wp.apply_fir(wp.FirFilter.from_taps(taps, 48000), w).samples
+    assert oracle.parity_error(y, oracle.fir_direct(taps, w.samples)) <= FIR_TOL
+
+
+def test_fir_tensor_core_zeros_and_tail():
+    w = wp.Wave(np.zeros((2, 9000)), 48000)
+    f = wp.design_fir("lp", 101, 1000, fs=48000)
+    assert np.array_equal(wp.apply_fir(f, w).samples, np.zeros((2, 9000)))
+    rng = np.random.default_rng(2)
+    for frames in (1, 7, 4095, 4096, 4097, 12289):
+        w = wp.Wave(rng.standard_normal((2, frames)), 48000)
+        y = wp.apply_fir(f, w).samples
+        assert oracle.parity_error(y, oracle.fir_direct(f.taps, w.samples)) <= FIR_TOL, frames
