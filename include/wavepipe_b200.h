@@ -120,6 +120,10 @@ const char *wp_last_error(void);
 int wp_abi_version(void);
 /* 0 if the current device can run this binary (sm_100), WP_EARCH otherwise */
 int wp_check_device(void);
+/* Diagnostics: when set, tensor-core chain launches record per-tile stage
+ * timestamps (%globaltimer, ns) into this device buffer ([tiles][12]) if it
+ * holds enough entries; NULL disables. Not for production use. */
+int wp_set_trace(uint64_t *device_buffer, size_t entries);
 /* Total kernel launches issued by this process through the library. */
 uint64_t wp_launch_count(void);
 

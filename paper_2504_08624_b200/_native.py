@@ -33,6 +33,7 @@ WP_IIR_PREC_F64 = 32
 # every symbol include/wavepipe_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "wp_plan_create",
+    "wp_set_trace",
     "wp_plan_destroy",
     "wp_plan_workspace_bytes",
     "wp_plan_execute",
@@ -97,9 +98,10 @@ def load(require_device: bool = False):
             lib.wp_peak_abs.argtypes = [vp, i64, i64, i64, vp, vp]
             lib.wp_last_error.restype = ctypes.c_char_p
             lib.wp_launch_count.restype = ctypes.c_uint64
+            lib.wp_set_trace.argtypes = [vp, sz]
             for name in ("wp_plan_create", "wp_plan_destroy", "wp_plan_workspace_bytes", "wp_plan_execute",
                          "wp_plan_num_passes", "wp_plan_launches", "wp_iir_cascade", "wp_fir",
-                         "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device"):
+                         "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace"):
                 getattr(lib, name).restype = ctypes.c_int
             _lib = lib
     if require_device:
@@ -123,6 +125,12 @@ def check(rc: int, what: str = "") -> None:
 def check_device() -> None:
     lib = load(require_device=True)
     check(lib.wp_check_device(), "device check")
+
+
+def set_trace(ptr: int, entries: int) -> None:
+    """Diagnostics: per-tile stage timestamps of tensor-core chain launches
+    into a device uint64 buffer (0 disables)."""
+    check(load().wp_set_trace(ptr or None, entries), "set_trace")
 
 
 def launch_count() -> int:

@@ -33,6 +33,8 @@ size_t fused_smem_bytes_f64(int S, int tpad);
 namespace {
 
 thread_local std::string g_err;
+unsigned long long *g_trace = nullptr;  // diagnostics: per-tile stage timestamps (wp_set_trace)
+size_t g_trace_entries = 0;
 std::atomic<unsigned long long> g_launches{0};
 std::atomic<unsigned long long> g_epoch{0};
 std::once_flag g_epoch_once;
@@ -103,6 +105,35 @@ void cascade_step(const std::vector<double> &sos, int S, const double *st, doubl
         out[2 * s + 1] = b2 * u - a2 * y;
         u = y;
     }
+}
+
+// Output of one DF2T cascade step (the last section's y) for state st, input u.
+double cascade_out(const std::vector<double> &sos, int S, const double *st, double u) {
+    for (int s = 0; s < S; ++s) {
+        const double y = sos[5 * s] * u + st[2 * s];
+        u = y;
+    }
+    return u;
+}
+
+// State space of the cascade: s' = A s + B u, y = C s + d u (DF2T states).
+void cascade_ss(const std::vector<double> &sos, int S, Mat &A, std::vector<double> &B, std::vector<double> &C,
+                double &d) {
+    const int D = 2 * S;
+    A.assign(D * D, 0.0);
+    B.assign(D, 0.0);
+    C.assign(D, 0.0);
+    std::vector<double> e(D), o(D);
+    for (int j = 0; j < D; ++j) {
+        std::fill(e.begin(), e.end(), 0.0);
+        e[j] = 1.0;
+        cascade_step(sos, S, e.data(), 0.0, o.data());
+        for (int i = 0; i < D; ++i) A[i * D + j] = o[i];
+        C[j] = cascade_out(sos, S, e.data(), 0.0);
+    }
+    std::fill(e.begin(), e.end(), 0.0);
+    cascade_step(sos, S, e.data(), 1.0, B.data());
+    d = cascade_out(sos, S, e.data(), 1.0);
 }
 
 void build_tables(wp::HostTables &t, const std::vector<double> &sos, int S, int H) {
@@ -194,6 +225,13 @@ struct Pass {
     int tc_Tp = 0, tc_K = 0, tc_W = 0;
     float tc_out_scale = 1.f;
     unsigned char *d_Bimg = nullptr;
+    // tensor-core chain (IIR [+ FIR] passes)
+    bool chain_tc = false;
+    int ct_H = 0, ct_K = 0, ct_W = 0;
+    float ct_out_scale = 1.f;
+    std::vector<double> ct_E;  // [64][D]
+    unsigned char *d_Bk = nullptr;  // int8 digit planes of the chunk-state weights
+    double ct_kscale[8] = {0};
     std::string desc;
     bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
 };
@@ -231,6 +269,144 @@ bool fir_tc_enabled() {
     return !(v && std::string(v) == "cuda");
 }
 
+bool chain_tc_enabled() {
+    const char *v = std::getenv("WP_CHAIN_IMPL");
+    return !(v && std::string(v) == "cuda");
+}
+
+// Build the tensor-core chain tables of pass p: combined response g (Toeplitz
+// B image, fp16 hi/lo), state-term matrix E, chunk-scan tables (M = A^64).
+int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
+    const int S = p.S, D = 2 * S;
+    Mat A;
+    std::vector<double> B, C;
+    double d = 0;
+    cascade_ss(p.sos, S, A, B, C, d);
+    double gain = (double)p.pre;
+    for (float g : p.post) gain *= (double)g;
+    std::vector<double> f = p.T > 0 ? p.taps : std::vector<double>{1.0};
+    const int T = (int)f.size();
+    // CA[t] = C A^t, t < H + 64
+    std::vector<double> CA((size_t)(H + 64) * D);
+    std::vector<double> row = C, nrow(D);
+    for (int t = 0; t < H + 64; ++t) {
+        for (int i = 0; i < D; ++i) CA[(size_t)t * D + i] = row[i];
+        for (int j = 0; j < D; ++j) {
+            long double acc = 0;
+            for (int i = 0; i < D; ++i) acc += (long double)row[i] * A[i * D + j];
+            nrow[j] = (double)acc;
+        }
+        row = nrow;
+    }
+    // impulse response h[t] = d (t = 0), C A^(t-1) B
+    std::vector<double> h(K);
+    h[0] = d;
+    for (int t = 1; t < K; ++t) {
+        long double acc = 0;
+        for (int i = 0; i < D; ++i) acc += (long double)CA[(size_t)(t - 1) * D + i] * B[i];
+        h[t] = (double)acc;
+    }
+    std::vector<double> g(K, 0.0);
+    for (int t = 0; t < K; ++t) {
+        long double acc = 0;
+        for (int k = 0; k < T && k <= t; ++k) acc += (long double)f[k] * h[t - k];
+        g[t] = (double)(acc * gain);
+    }
+    p.ct_E.assign(64 * D, 0.0);
+    for (int q = 0; q < 64; ++q)
+        for (int i = 0; i < D; ++i) {
+            long double acc = 0;
+            for (int k = 0; k < T; ++k) acc += (long double)f[k] * CA[(size_t)(H + q - k) * D + i];
+            p.ct_E[q * D + i] = (double)(acc * gain);
+        }
+    // B image: B[q, k] = g[q + H - k], K-major SW128, fp16 hi / lo (x 2^11)
+    double gmax = 0;
+    for (double v : g) gmax = std::max(gmax, std::fabs(v));
+    int ex = 0;
+    if (gmax > 0) std::frexp(gmax, &ex);
+    const int fB = gmax > 0 ? 14 - ex : 0;
+    p.ct_out_scale = (float)std::ldexp(1.0, -fB);
+    const int atoms = (K + 63) / 64;
+    const size_t split = (size_t)atoms * 8192 / sizeof(__half);
+    std::vector<__half> img(2 * split, __float2half_rn(0.f));
+    for (int q = 0; q < 64; ++q)
+        for (int k = 0; k < K; ++k) {
+            const int t = q + H - k;
+            const float val = (t >= 0 && t < K) ? (float)std::ldexp(g[t], fB) : 0.f;
+            const __half hi = __float2half_rn(val);
+            const __half lo = __float2half_rn(val - __half2float(hi));  // unscaled: one accumulator
+            const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
+            const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
+            img[phys / 2] = hi;
+            img[split + phys / 2] = lo;
+        }
+    cudaError_t e = cudaMalloc(&p.d_Bimg, img.size() * sizeof(__half));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");
+    e = cudaMemcpy(p.d_Bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(Bimg)");
+    // chunk-scan tables: K[n] = A^(63-n) B, M = A^64, tiles of 128 chunks
+    build_tables(p.tables, p.sos, S, 0);
+    // exact e-GEMM operand: K[n][d] as 31-bit fixed point per state d, 4 int8
+    // digits (top digit signed), K-major no-swizzle rows of 64 bytes
+    {
+        std::vector<unsigned char> bk((size_t)wpk::CT_KD * 1024, 0);
+        for (int d = 0; d < D; ++d) {
+            double kmax = 0;
+            for (int n = 0; n < 64; ++n) kmax = std::max(kmax, std::fabs(p.tables.K[n * D + d]));
+            int kex = 0;
+            if (kmax > 0) std::frexp(kmax, &kex);
+            const int kappa = kmax > 0 ? 30 - kex : 0;
+            p.ct_kscale[d] = std::ldexp(1.0, -kappa);
+            for (int n = 0; n < 64; ++n) {
+                const long long q = std::llround(std::ldexp(p.tables.K[n * D + d], kappa));
+                const uint32_t u = (uint32_t)(int32_t)q;
+                for (int b = 0; b < wpk::CT_KD; ++b)
+                    bk[(size_t)b * 1024 + wpk::ctd::dg_off(d, n)] = (unsigned char)((u >> (8 * b)) & 255u);
+            }
+        }
+        cudaError_t e2 = cudaMalloc(&p.d_Bk, bk.size());
+        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaMalloc(Bk)");
+        e2 = cudaMemcpy(p.d_Bk, bk.data(), bk.size(), cudaMemcpyHostToDevice);
+        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaMemcpy(Bk)");
+    }
+    const size_t es = f64 ? sizeof(double) : sizeof(float);
+    std::vector<unsigned char> gbuf(es * D * D * 33), tbuf(es * 33 * D * D);
+    for (size_t i = 0; i < p.tables.G.size(); ++i) {
+        if (f64)
+            reinterpret_cast<double *>(gbuf.data())[i] = p.tables.G[i];
+        else
+            reinterpret_cast<float *>(gbuf.data())[i] = (float)p.tables.G[i];
+    }
+    for (size_t i = 0; i < p.tables.TP.size(); ++i) {
+        if (f64)
+            reinterpret_cast<double *>(tbuf.data())[i] = p.tables.TP[i];
+        else
+            reinterpret_cast<float *>(tbuf.data())[i] = (float)p.tables.TP[i];
+    }
+    e = cudaMalloc(&p.d_G, gbuf.size());
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(G)");
+    e = cudaMalloc(&p.d_TP, tbuf.size());
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(TP)");
+    e = cudaMemcpy(p.d_G, gbuf.data(), gbuf.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(G)");
+    e = cudaMemcpy(p.d_TP, tbuf.data(), tbuf.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(TP)");
+    p.chain_tc = true;
+    p.f64 = f64;
+    p.ct_H = H;
+    p.ct_K = K;
+    p.ct_W = W;
+    p.smem = smem;
+    p.grid_cap = wp::sm_count();
+    p.Lout = wpk::CT_TOUT;
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "chain_tc[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3 M128xN64 K=%d halo=%d tile=%d smem=%zu",
+             (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
+    p.desc = buf;
+    return WP_OK;
+}
+
 int finalize_pass(Pass &p) {
     if (p.kind != Pass::FUSED) {
         char buf[128];
@@ -244,6 +420,23 @@ int finalize_pass(Pass &p) {
         p.tc_K = (p.tc_Tp + wpk::TC_N + 15) / 16 * 16;
         p.tc_W = wpk::TC_N * (wpk::TC_M - 1) + p.tc_K;
         p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
+    }
+    if (p.S > 0 && chain_tc_enabled()) {
+        const int T = p.T > 0 ? p.T : 1;
+        const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
+        const int K = H + 64;
+        const int W = wpk::CT_TOUT + H;
+        if (H <= wpk::CT_MAX_H) {
+        double rmax = 0;
+        for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
+        const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
+        const size_t smem = wp::chain_tc_smem_bytes(W, K, p.S, f64);
+        if (W / 4 <= wpk::CT_QMAX * wpk::CT_CONV && smem <= 227 * 1024) {
+            int rc = build_chain_tc(p, H, K, W, f64, smem);
+            if (rc != WP_OK) return rc;
+            return WP_OK;
+        }
+        }
     }
     if (p.fir_tc) {
         double hmax = 0;
@@ -345,6 +538,8 @@ int finalize_pass(Pass &p) {
 void free_pass(Pass &p) {
     if (p.d_Bimg) cudaFree(p.d_Bimg);
     p.d_Bimg = nullptr;
+    if (p.d_Bk) cudaFree(p.d_Bk);
+    p.d_Bk = nullptr;
     if (p.d_G) cudaFree(p.d_G);
     if (p.d_TP) cudaFree(p.d_TP);
     if (p.d_taps) cudaFree(p.d_taps);
@@ -390,6 +585,11 @@ const char *wp_last_error(void) { return g_err.c_str(); }
 int wp_abi_version(void) { return 1; }
 uint64_t wp_launch_count(void) { return (uint64_t)g_launches.load(); }
 int wp_check_device(void) { return arch_ok(); }
+int wp_set_trace(uint64_t *device_buffer, size_t entries) {
+    g_trace = reinterpret_cast<unsigned long long *>(device_buffer);
+    g_trace_entries = device_buffer ? entries : 0;
+    return WP_OK;
+}
 
 int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan) {
     if (!out_plan) return fail(WP_EINVAL, "out_plan is NULL");
@@ -568,6 +768,37 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             if (e != cudaSuccess) return cuda_fail(e, "peak_abs launch");
             e = wp::launch_scale_by_peak(in, out, C, N, ld_in, ld_out, peak, (float)p.target, stream);
             if (e != cudaSuccess) return cuda_fail(e, "scale launch");
+        } else if (p.chain_tc) {
+            wpk::ChainTcArgs a{};
+            a.x = in;
+            a.y = out;
+            a.C = C;
+            a.N = N;
+            a.ldx = ld_in;
+            a.ldy = ld_out;
+            a.total_tiles = ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C;
+            if (a.total_tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
+            a.H = p.ct_H;
+            a.K = p.ct_K;
+            a.W = p.ct_W;
+            a.Bimg = p.d_Bimg;
+            a.Bk = p.d_Bk;
+            for (int d = 0; d < 8; ++d) a.kscale[d] = p.ct_kscale[d];
+            a.out_scale = p.ct_out_scale;
+            a.G = p.d_G;
+            a.TP = p.d_TP;
+            a.recs = ws + rec_off;
+            a.epoch = next_epoch();
+            a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+            a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+            {
+                const char *dv = std::getenv("WP_CT_DBG");
+                a.dbg = dv ? std::atoi(dv) : 0;
+            }
+            a.trace = (g_trace && g_trace_entries >= (size_t)a.total_tiles * wpk::CT_TRACE_EV) ? g_trace : nullptr;
+            const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
+            e = wp::launch_chain_tc(p.f64, p.S, a, p.tables, p.ct_E, grid, p.smem, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "chain_tc launch");
         } else if (p.fir_tc) {
             wpk::FirTcArgs a{};
             a.x = in;

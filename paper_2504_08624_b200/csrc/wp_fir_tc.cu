@@ -93,8 +93,9 @@ __device__ __forceinline__ Geo geo(const FirTcArgs &a, long long tile) {
 __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the operand buffers (swizzle phase = address bits)
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align by offsetting the __shared__ array itself (keeps the shared
+    // address space visible to the compiler: LDS/STS, not generic LD/ST)
+    unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nk = a.K / 16;
     // ---- shared memory carve-up ----

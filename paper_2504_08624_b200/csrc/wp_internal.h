@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "wp_chain_tc.cuh"
 #include "wp_fused.cuh"
 
 namespace wpk {
@@ -68,6 +69,11 @@ cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long lon
 size_t fir_tc_smem_bytes(int W, int K);
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
 int fir_tc_occupancy(size_t smem);
+
+// tensor-core chain (wp_chain_tc.cu)
+size_t chain_tc_smem_bytes(int W, int K, int S, bool f64);
+cudaError_t launch_chain_tc(bool f64, int S, const wpk::ChainTcArgs &a, const HostTables &t,
+                            const std::vector<double> &E, int grid, size_t smem, cudaStream_t st);
 
 void count_launch(int n = 1);
 int sm_count();
