@@ -630,17 +630,26 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                     delete plan;
                     return fail(WP_EINVAL, "IIR stage needs >= 1 section");
                 }
+                // Exact no-op sections (b = (1,0,0), a = (0,0); e.g. design_peaking
+                // at 0 dB, design.py:437-438) are dropped: the reference's DF2T
+                // passes samples through them bit for bit (y = 1*x + 0).
+                std::vector<int> keep;
+                for (int k = 0; k < st.n; ++k) {
+                    const double *r = st.coef + 5 * k;
+                    if (!(r[0] == 1.0 && r[1] == 0.0 && r[2] == 0.0 && r[3] == 0.0 && r[4] == 0.0)) keep.push_back(k);
+                }
+                if (keep.empty()) break;
                 if (cur.T > 0 || !cur.post.empty()) close();
-                int idx = 0;
-                while (idx < st.n) {
+                size_t idx = 0;
+                while (idx < keep.size()) {
                     int room = wpk::MAXS - cur.S;
                     if (room == 0) {
                         close();
                         room = wpk::MAXS;
                     }
-                    const int take = std::min(room, st.n - idx);
+                    const int take = std::min<int>(room, (int)(keep.size() - idx));
                     for (int s = 0; s < take; ++s)
-                        for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * (idx + s) + j]);
+                        for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * keep[idx + s] + j]);
                     cur.S += take;
                     cur.prec_flag |= st.flags & (WP_IIR_PREC_F32 | WP_IIR_PREC_F64);
                     idx += take;
