@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
     TS *Ps = reinterpret_cast<TS *>(smem + lay.tabs);  // [5][D][D]
     TS *Ws = Ps + 5 * D * D;                           // [4][D][D]
     TS *MTs = Ws + 4 * D * D;                          // [D][D]
-    TS *Es = MTs + D * D;                              // E transposed: [D][64]
+    // E transposed, split into fp32 hi / lo parts: Esh[D][64], Esl[D][64]
+    float *Esh = reinterpret_cast<float *>(MTs + D * D);
+    float *Esl = Esh + D * 64;
     TS *sbuf = reinterpret_cast<TS *>(smem + lay.sbuf);
     unsigned char *stg = smem + lay.stg;
     TS *warp_incl = reinterpret_cast<TS *>(smem + lay.misc);  // [2][4][D]
@@ -286,7 +288,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
             for (int t = 0; t < 4; ++t) Ws[t * D * D + i] = tb.W[t][r][q];
             MTs[i] = tb.MT[r][q];
         }
-        for (int i = tid; i < 64 * D; i += CT_THREADS) Es[i] = et.E[i % 64][i / 64];  // transposed [D][64]
+        for (int i = tid; i < 64 * D; i += CT_THREADS) {
+            const double e = (double)et.E[i % 64][i / 64];
+            Esh[i] = (float)e;
+            Esl[i] = (float)(e - (double)(float)e);
+        }
     }
     wptc::fence_proxy_async_smem();
     wptc::fence_before_sync();
@@ -378,13 +384,20 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
             float m = 0.f;
             const bool interior = a.vec_x && start >= 0 && start + a.W <= a.N;
 #pragma unroll
-            for (int j = 0; j < CT_QMAX; ++j) {
-                const int q = ct + j * CT_CONV;
-                if (q < nq) {
-                    const long long p0 = start + 4LL * q;
-                    v[j] = interior ? __ldcs(reinterpret_cast<const float4 *>(xr + p0)) : load_region4(xr, p0, a.N, a.vec_x);
-                } else {
-                    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (interior) {
+                const float4 *src4 = reinterpret_cast<const float4 *>(xr + start) + ct;
+#pragma unroll
+                for (int j = 0; j < CT_QMAX; ++j)
+                    v[j] = (ct + j * CT_CONV < nq) ? __ldcs(src4 + j * CT_CONV) : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+#pragma unroll 1
+                for (int j = 0; j < CT_QMAX; ++j) {
+                    const int q = ct + j * CT_CONV;
+                    const float4 t = q < nq ? load_region4(xr, start + 4LL * q, a.N, a.vec_x) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    // register arrays need static indices: select into place
+#pragma unroll
+                    for (int jj = 0; jj < CT_QMAX; ++jj)
+                        if (jj == j) v[jj] = t;
                 }
             }
 #pragma unroll
@@ -663,6 +676,12 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
             for (int d = 0; d < D; ++d) V[d] = cv_s[(s * 4 + wq) * D + d];
             ctd::arrive(CBAR(CV_EMPTY, s));
             ctd::matvec_tree<D, TS>(sv, V, [&](int r, int q) { return gsm[(lt_off(r) + q) * 32 + lane]; });
+            float sh[D], sl[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                sh[d] = (float)sv[d];
+                sl[d] = (float)(sv[d] - (TS)sh[d]);
+            }
             wptc::mbar_wait(CBAR(ACC_FULL, s3), (uint32_t)((i / 3) & 1));
             wptc::fence_after_sync();
             if (row == 0 && a.trace) a.trace[tile * CT_TRACE_EV + 7] = ctd::gtimer();
@@ -679,32 +698,48 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
                     wptc::fence_before_sync();
                     ctd::arrive(CBAR(ACC_EMPTY, s3));
                 }
-                TS acc[16];
+                // state term in fp32 double-single: E s = Eh sh + (El sh + Eh sl)
+                // (no fp64 <-> fp32 conversions per output; error ~2^-24 |E s|)
+                float acc[16], cor[16];
 #pragma unroll
-                for (int pp = 0; pp < 16; ++pp) acc[pp] = TS(t16[pp] * osc);
+                for (int pp = 0; pp < 16; ++pp) {
+                    acc[pp] = t16[pp] * osc;
+                    cor[pp] = 0.f;
+                }
                 if (!(a.dbg & 4)) {
 #pragma unroll
                     for (int d = 0; d < D; ++d) {
-                        const TS *er = Es + d * 64 + 16 * ch;  // uniform address: broadcast loads
+                        const float4 *eh = reinterpret_cast<const float4 *>(Esh + d * 64 + 16 * ch);  // uniform: broadcast
+                        const float4 *el = reinterpret_cast<const float4 *>(Esl + d * 64 + 16 * ch);
 #pragma unroll
-                        for (int pp = 0; pp < 16; ++pp) acc[pp] = fma(er[pp], sv[d], acc[pp]);
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 h4 = eh[q4], l4 = el[q4];
+                            const float hv[4] = {h4.x, h4.y, h4.z, h4.w}, lv4[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                acc[4 * q4 + u] = fmaf(hv[u], sh[d], acc[4 * q4 + u]);
+                                if constexpr (sizeof(TS) == 8)
+                                    cor[4 * q4 + u] = fmaf(lv4[u], sh[d], fmaf(hv[u], sl[d], cor[4 * q4 + u]));
+                            }
+                        }
                     }
                 }
                 float4 *dst = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4)
-                    dst[q4] = make_float4(float(acc[4 * q4]), float(acc[4 * q4 + 1]), float(acc[4 * q4 + 2]),
-                                          float(acc[4 * q4 + 3]));
+                    dst[q4] = make_float4(acc[4 * q4] + cor[4 * q4], acc[4 * q4 + 1] + cor[4 * q4 + 1],
+                                          acc[4 * q4 + 2] + cor[4 * q4 + 2], acc[4 * q4 + 3] + cor[4 * q4 + 3]);
                 if (hh == 1) {
                     __syncwarp();
                     // 32 rows x 32 outputs of this half: 8 float4 per row, 4 rows per instruction
-#pragma unroll 2
+                    const long long tleft = a.N - n0;  // valid outputs in this tile
+#pragma unroll 1
                     for (int r = 0; r < 8; ++r) {
                         const int q = lane + 32 * r;
                         const int rr = q >> 3, c4 = q & 7;
                         const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * CT_STG_PITCH + 16 * c4);
-                        const long long o = 64LL * (32 * wq + rr) + 32 * h + 4 * c4;  // offset from n0
-                        const long long left = a.N - n0 - o;
+                        const int o = 64 * (32 * wq + rr) + 32 * h + 4 * c4;  // offset from n0
+                        const long long left = tleft - o;
                         if (a.vec_y && left >= 4) {
                             __stcs(reinterpret_cast<float4 *>(yr + o), v);
                         } else {

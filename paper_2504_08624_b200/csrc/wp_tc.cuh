@@ -75,13 +75,17 @@ __device__ __forceinline__ void mbar_init(uint32_t saddr, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Blocking wait on an mbarrier phase. The suspend-time hint lets the waiting
+// warp sleep in hardware until the phase completes instead of re-polling the
+// barrier (spinning warps otherwise eat issue slots and shared-memory pipe
+// bandwidth that the producer warps need).
 __device__ __forceinline__ void mbar_wait(uint32_t saddr, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n\t}\n" ::"r"(saddr),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 
