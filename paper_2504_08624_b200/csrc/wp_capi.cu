@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <complex>
 #include <cstdlib>
 #include <unistd.h>
 
@@ -225,6 +226,10 @@ struct Pass {
     int tc_Tp = 0, tc_K = 0, tc_W = 0;
     float tc_out_scale = 1.f;
     unsigned char *d_Bimg = nullptr;
+    // FFT overlap-save (long FIR-only passes)
+    bool fft = false;
+    int fft_Tpad = 0;
+    float2 *d_H = nullptr, *d_tw = nullptr;
     // tensor-core chain (IIR [+ FIR] passes)
     bool chain_tc = false;
     int ct_H = 0, ct_K = 0, ct_W = 0;
@@ -407,6 +412,70 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
     return WP_OK;
 }
 
+// Iterative radix-2 FFT in float64 (plan time only), in place, forward.
+void host_fft(std::vector<std::complex<double>> &a) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const double ang = -2.0 * M_PI / (double)len;
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const std::complex<double> w(std::cos(ang * (double)k), std::sin(ang * (double)k));
+                const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
+// FFT overlap-save tables of pass p: spectrum of the (gain-scaled) taps in the
+// kernel's digit-reversed order k = k1 + 32 k2 + 1024 k3 -> [k3][k1*32 + k2],
+// pre-divided by M, and the two-level twiddle table.
+int build_fft(Pass &p) {
+    const int M = wpk::FFT_M;
+    const int Tpad = (p.T - 1 + 511) / 512 * 512;
+    if (Tpad >= M - 512) return fail(WP_EUNSUP, "FIR too long for the FFT overlap-save path (taps <= 15361)");
+    double gain = (double)p.pre;
+    for (float g : p.post) gain *= (double)g;
+    std::vector<std::complex<double>> h(M, 0.0);
+    for (int i = 0; i < p.T; ++i) h[i] = p.taps[i] * gain / (double)M;
+    host_fft(h);
+    std::vector<float2> Hp(M), tw(256);
+    for (int k3 = 0; k3 < 16; ++k3)
+        for (int k1 = 0; k1 < 32; ++k1)
+            for (int k2 = 0; k2 < 32; ++k2) {
+                const std::complex<double> v = h[k1 + 32 * k2 + 1024 * k3];
+                Hp[k3 * 1024 + k1 * 32 + k2] = make_float2((float)v.real(), (float)v.imag());
+            }
+    for (int i = 0; i < 128; ++i) {
+        const double a1 = -2.0 * M_PI * i / M, a2 = -2.0 * M_PI * 128.0 * i / M;
+        tw[i] = make_float2((float)std::cos(a1), (float)std::sin(a1));
+        tw[128 + i] = make_float2((float)std::cos(a2), (float)std::sin(a2));
+    }
+    cudaError_t e = cudaMalloc(&p.d_H, sizeof(float2) * M);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(H)");
+    e = cudaMemcpy(p.d_H, Hp.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(H)");
+    e = cudaMalloc(&p.d_tw, sizeof(float2) * 256);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tw)");
+    e = cudaMemcpy(p.d_tw, tw.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tw)");
+    p.fft = true;
+    p.fft_Tpad = Tpad;
+    p.Lout = M - Tpad;
+    p.grid_cap = wp::sm_count();
+    char buf[256];
+    snprintf(buf, sizeof buf, "fft_ols[pre=%g taps=%d post=%zu] M=%d halo=%d block=%d 2 ch/CTA smem=%zu", (double)p.pre, p.T,
+             p.post.size(), M, Tpad, M - Tpad, wp::fft_ols_smem_bytes());
+    p.desc = buf;
+    return WP_OK;
+}
+
 int finalize_pass(Pass &p) {
     if (p.kind != Pass::FUSED) {
         char buf[128];
@@ -437,6 +506,10 @@ int finalize_pass(Pass &p) {
             return WP_OK;
         }
         }
+    }
+    if (p.S == 0 && p.T > 1 && !(p.fir_flags & WP_FIR_DIRECT) && ((p.fir_flags & WP_FIR_FFT) || !p.fir_tc)) {
+        p.fir_tc = false;
+        return build_fft(p);
     }
     if (p.fir_tc) {
         double hmax = 0;
@@ -540,6 +613,9 @@ void free_pass(Pass &p) {
     p.d_Bimg = nullptr;
     if (p.d_Bk) cudaFree(p.d_Bk);
     p.d_Bk = nullptr;
+    if (p.d_H) cudaFree(p.d_H);
+    if (p.d_tw) cudaFree(p.d_tw);
+    p.d_H = p.d_tw = nullptr;
     if (p.d_G) cudaFree(p.d_G);
     if (p.d_TP) cudaFree(p.d_TP);
     if (p.d_taps) cudaFree(p.d_taps);
@@ -664,6 +740,7 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                 if (cur.T > 0 || !cur.post.empty()) close();
                 cur.T = st.n;
                 cur.taps.assign(st.coef, st.coef + st.n);
+                cur.fir_flags = st.flags & (WP_FIR_DIRECT | WP_FIR_FFT);
                 break;
             }
             case WP_STAGE_NORMALIZE: {
@@ -777,6 +854,23 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             if (e != cudaSuccess) return cuda_fail(e, "peak_abs launch");
             e = wp::launch_scale_by_peak(in, out, C, N, ld_in, ld_out, peak, (float)p.target, stream);
             if (e != cudaSuccess) return cuda_fail(e, "scale launch");
+        } else if (p.fft) {
+            wpk::FftArgs a{};
+            a.x = in;
+            a.y = out;
+            a.C = C;
+            a.N = N;
+            a.ldx = ld_in;
+            a.ldy = ld_out;
+            a.Tpad = p.fft_Tpad;
+            a.L = p.Lout;
+            a.nblk = (N + a.L - 1) / a.L;
+            a.total = a.nblk * ((C + 1) / 2);
+            a.H = p.d_H;
+            a.tw = p.d_tw;
+            const int grid = (int)std::min<long long>(a.total, p.grid_cap);
+            e = wp::launch_fft_ols(a, grid, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
         } else if (p.chain_tc) {
             wpk::ChainTcArgs a{};
             a.x = in;

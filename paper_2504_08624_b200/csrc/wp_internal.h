@@ -31,6 +31,20 @@ struct FirTcArgs {
     int vec_x, vec_y;
 };
 
+constexpr int FFT_M = 16384;      // complex FFT size of the overlap-save path
+constexpr int FFT_THREADS = 512;
+
+struct FftArgs {
+    const float *x;
+    float *y;
+    long long C, N, ldx, ldy;
+    long long nblk;    // blocks per channel
+    long long total;   // work items: channel pairs x blocks
+    int Tpad, L;       // halo (multiple of 512, >= taps-1), new outputs per block
+    const float2 *H;   // [16][1024] spectrum of the taps, digit-reversed order, x gain / M
+    const float2 *tw;  // [256] W_M^n (n < 128), W_M^(128 k) (k < 128)
+};
+
 }  // namespace wpk
 
 namespace wp {
@@ -74,6 +88,10 @@ int fir_tc_occupancy(size_t smem);
 size_t chain_tc_smem_bytes(int W, int K, int S, bool f64);
 cudaError_t launch_chain_tc(bool f64, int S, const wpk::ChainTcArgs &a, const HostTables &t,
                             const std::vector<double> &E, int grid, size_t smem, cudaStream_t st);
+
+// FFT overlap-save long FIR (wp_fft_ols.cu)
+size_t fft_ols_smem_bytes();
+cudaError_t launch_fft_ols(const wpk::FftArgs &a, int grid, cudaStream_t st);
 
 void count_launch(int n = 1);
 int sm_count();
