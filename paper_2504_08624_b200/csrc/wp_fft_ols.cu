@@ -89,6 +89,23 @@ __device__ __forceinline__ float2 twid(const float2 *tw, int n) {  // W_M^n, 0 <
     return cmul(tw[n & 127], tw[128 + (n >> 7)]);
 }
 
+// v[k] *= W_M^(base k) (INV: conjugate) for k < 32, with v[k] addressed through
+// brev: powers re-anchored from the table every 8 steps (<= ~8 ulp).
+template <bool INV, bool BREV>
+__device__ __forceinline__ void twiddle32(float2 (&v)[32], const float2 *tw, int base) {
+    const float2 w1 = twid(tw, base);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        float2 w = twid(tw, base * 8 * g);
+#pragma unroll
+        for (int k = 8 * g; k < 8 * g + 8; ++k) {
+            const int idx = BREV ? brev(k, 5) : k;
+            if (k > 0) v[idx] = INV ? cmulc(v[idx], w) : cmul(v[idx], w);
+            w = cmul(w, w1);
+        }
+    }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
@@ -107,29 +124,33 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         const float *x0 = a.x + c0 * a.ldx, *x1 = a.x + (has1 ? c1 : c0) * a.ldx;
         float2 v[32];
         const bool interior = s >= 0 && s + FM <= a.N;
+        if (interior) {
+            const float *p0 = x0 + s + t, *p1 = x1 + s + t;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const long long n = s + t + 512 * j;
-            if (interior) {
-                v[j] = make_float2(__ldcs(x0 + n), has1 ? __ldcs(x1 + n) : 0.f);
-            } else {
+            for (int j = 0; j < 32; ++j) v[j] = make_float2(__ldcs(p0 + 512 * j), has1 ? __ldcs(p1 + 512 * j) : 0.f);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const long long n = s + t + 512 * j;
                 const bool ok = n >= 0 && n < a.N;
                 v[j] = make_float2(ok ? x0[n] : 0.f, (ok && has1) ? x1[n] : 0.f);
             }
         }
         // ---- forward pass 1: DFT32 over j, twiddle W_M^(t k1) -> buf[k1*512 + t] ----
         fft_reg<32, false>(v);
+        twiddle32<false, true>(v, tws, t);
         __syncthreads();  // previous block's last reads of buf are done
 #pragma unroll
-        for (int k1 = 0; k1 < 32; ++k1) buf[k1 * 512 + t] = cmul(v[brev(k1, 5)], twid(tws, t * k1));
+        for (int k1 = 0; k1 < 32; ++k1) buf[k1 * 512 + t] = v[brev(k1, 5)];
         __syncthreads();
         // ---- forward pass 2: thread (k1p, bp): DFT32 over c, twiddle W_512^(b k2) ----
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = buf[k1p * 512 + bp + 16 * c];
         fft_reg<32, false>(v);
+        twiddle32<false, true>(v, tws, 32 * bp);
         __syncthreads();
 #pragma unroll
-        for (int k2 = 0; k2 < 32; ++k2) buf[17 * (k1p * 32 + k2) + bp] = cmul(v[brev(k2, 5)], twid(tws, 32 * bp * k2));
+        for (int k2 = 0; k2 < 32; ++k2) buf[17 * (k1p * 32 + k2) + bp] = v[brev(k2, 5)];
         __syncthreads();
         // ---- pass 3 + pointwise product + inverse pass 3 (registers only) ----
 #pragma unroll 1
@@ -149,7 +170,8 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         __syncthreads();
         // ---- inverse pass 2: conj twiddle, IDFT32 over k2 -> c ----
 #pragma unroll
-        for (int k2 = 0; k2 < 32; ++k2) v[k2] = cmulc(buf[17 * (k1p * 32 + k2) + bp], twid(tws, 32 * bp * k2));
+        for (int k2 = 0; k2 < 32; ++k2) v[k2] = buf[17 * (k1p * 32 + k2) + bp];
+        twiddle32<true, false>(v, tws, 32 * bp);
         fft_reg<32, true>(v);
         __syncthreads();
 #pragma unroll
@@ -157,19 +179,21 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         __syncthreads();
         // ---- inverse pass 1: conj twiddle W_M^(t k1), IDFT32 over k1 -> j ----
 #pragma unroll
-        for (int k1 = 0; k1 < 32; ++k1) v[k1] = cmulc(buf[k1 * 512 + t], twid(tws, t * k1));
+        for (int k1 = 0; k1 < 32; ++k1) v[k1] = buf[k1 * 512 + t];
+        twiddle32<true, false>(v, tws, t);
         fft_reg<32, true>(v);
         // outputs n = t + 512 j >= Tpad of this block (1/M folded into H)
         float *y0 = a.y + c0 * a.ldy, *y1 = a.y + (has1 ? c1 : c0) * a.ldy;
         const long long o0 = blk * a.L - a.Tpad;  // output index of window position 0
+        float *q0 = y0 + o0 + t, *q1 = y1 + o0 + t;
+        const long long lim = a.N - o0 - t;  // valid while 512 j < lim
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             const int n = t + 512 * j;
-            const long long o = o0 + n;
-            if (n >= a.Tpad && o < a.N) {
+            if (n >= a.Tpad && 512LL * j < lim) {
                 const float2 r = v[brev(j, 5)];
-                __stcs(y0 + o, r.x);
-                if (has1) __stcs(y1 + o, r.y);
+                __stcs(q0 + 512 * j, r.x);
+                if (has1) __stcs(q1 + 512 * j, r.y);
             }
         }
     }
