@@ -346,6 +346,10 @@ def main():
 
     hbm_peak, bf16_peak, peak_kind = load_peaks()
     algo_bytes = 8.0 * units  # fp32 read once + write once per channel-sample
+    passes = plan.describe()
+    kernel_names = {"chain_tc": "wpk::chain_tc_kernel", "fir_tc": "wpk::fir_tc_kernel",
+                    "fft_ols": "wpk::fft_ols_kernel", "fused": "wpk::fused_chain_kernel"}
+    kernels = [kernel_names.get(d.split("[")[0], d.split("[")[0]) for d in passes]
     achieved = algo_bytes / (per_launch_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -370,11 +374,11 @@ def main():
         "data": "synthetic white noise generated on device (reference generator, seed 42+rank)",
         "config": {"workload": cfg["workload"], "config_id": name, "channels_per_gpu": C, "frames": N, "fs": fs,
                    "l2": "inputs larger than L2 (737 MB in + 737 MB out per step), no flush",
-                   "passes": plan.describe(), "parallelism": f"channel batches x{world}, no collectives"},
+                   "passes": passes, "parallelism": f"channel batches x{world}, no collectives"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": per_launch_ms,
-                     "kernel": "wpk::fused_chain_kernel (one launch per step)"},
+                     "kernel": " + ".join(kernels) + f" ({plan.launches()} launch(es) per step)"},
         "e2e": {"value": units * world / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,
                 "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned)"},
@@ -382,6 +386,14 @@ def main():
         "clocks": clocks,
         "parity_check": {"max_abs_err_over_peak": parity, "sample": f"ch0 first {n_chk} frames vs oracle"},
     }
+    taps = sum(len(getattr(st, "taps", ())) for st in stages)
+    if any(k in ("wpk::chain_tc_kernel", "wpk::fir_tc_kernel") for k in kernels) and taps:
+        # algorithmic FIR flops = 2 T per channel-sample, against
+        # the dense fp16 tensor peak; the fp16 x3 split runs 3x those MMAs
+        tflops = 2.0 * taps * units / (per_launch_ms / 1e3) / 1e12
+        line["roofline"]["tensor"] = {"achieved_tflops": tflops, "peak_tflops": bf16_peak,
+                                      "frac": tflops / bf16_peak, "split_overhead": 3,
+                                      "note": "algorithmic 2*T flops/ch-sample; executed MMA work is 3x (fp16 hi/lo split)"}
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(name, wp)
     print(json.dumps(line), flush=True)
