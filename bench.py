@@ -378,7 +378,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": per_launch_ms,
-                     "kernel": " + ".join(kernels) + f" ({plan.launches()} launch(es) per step)"},
+                     "kernel": " + ".join(kernels) + f" ({plan.launches} launch(es) per step)"},
         "e2e": {"value": units * world / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,
                 "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned)"},

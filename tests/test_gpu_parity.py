@@ -313,3 +313,26 @@ def test_fir_tensor_core_zeros_and_tail():
         w = wp.Wave(rng.standard_normal((2, frames)), 48000)
         y = wp.apply_fir(f, w).samples
         assert oracle.parity_error(y, oracle.fir_direct(f.taps, w.samples)) <= FIR_TOL, frames
+
+
+# ---- kernel selection: the headline configs run on the intended kernels -----
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize(
+    "stages, fs, kernel",
+    [
+        (lambda: [wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
+                  wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, "chain_tc"),   # cfg3
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, "chain_tc"),              # cfg5
+        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, "chain_tc"),              # cfg1
+        (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, "fir_tc"),            # cfg2
+        (lambda: [wp.design_fir("lp", 4096, 2000, "hamming")], 48000, "fft_ols"),          # cfg4
+    ],
+)
+def test_plan_uses_intended_kernel(stages, fs, kernel):
+    from paper_2504_08624_b200 import engine
+
+    plan = engine.plan_for(wp.Chain(stages()).bind(fs).stages, device=0)
+    desc = plan.describe()
+    assert len(desc) == 1 and desc[0].startswith(kernel), desc
