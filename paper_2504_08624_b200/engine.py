@@ -253,6 +253,69 @@ def execute_entries(entries, src, out=None):
     return out
 
 
+_streams = {}
+
+
+def _copy_streams(device):
+    import torch
+
+    key = device.index
+    if key not in _streams:
+        with torch.cuda.device(device):
+            _streams[key] = (torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device))
+    return _streams[key]
+
+
+def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 0):
+    """Host -> device -> host execution of a recorded chain, overlapped.
+
+    ``host_src`` and ``host_out`` are pinned float32 CPU tensors ``[C, N]``.
+    Channels are cut into pair-aligned blocks (channels are independent, and
+    the FFT path filters pairs together, so results are bit-identical to one
+    launch over all channels); block b's upload, the fused pass over block
+    b-1 and block b-2's download run concurrently on three streams, so the
+    PCIe link carries both directions at once instead of one after the other.
+    """
+    import torch
+
+    from ._native import _require_cuda
+    from .sharding import partition
+
+    _require_cuda()
+    C, N = host_src.shape
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    nblk = blocks or max(1, min((C + 1) // 2, 32))
+    parts = [(a, b) for a, b in partition(C, nblk) if b > a]
+    with torch.cuda.device(dev):
+        s_in, s_run, s_out = _copy_streams(dev)
+        x = torch.empty((C, N), dtype=torch.float32, device=dev)
+        y = torch.empty_like(x)
+        plan = _plans.get(dev.index, entries)
+        ws = _workspace(dev, s_run.cuda_stream, max(plan.workspace_bytes(b - a, N) for a, b in parts))
+        cur = torch.cuda.current_stream(dev)
+        s_in.wait_stream(cur)
+        for a, b in parts:
+            with torch.cuda.stream(s_in):
+                x[a:b].copy_(host_src[a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            s_run.wait_event(ev_in)
+            plan.execute(x[a:b].data_ptr(), y[a:b].data_ptr(), b - a, N, N, N, ws.data_ptr(), ws.numel(),
+                         s_run.cuda_stream)
+            ev_run = torch.cuda.Event()
+            ev_run.record(s_run)
+            s_out.wait_event(ev_run)
+            with torch.cuda.stream(s_out):
+                host_out[a:b].copy_(y[a:b], non_blocking=True)
+        # keep the device buffers alive until the streams are done with them
+        x.record_stream(s_in)
+        x.record_stream(s_run)
+        y.record_stream(s_run)
+        y.record_stream(s_out)
+        s_out.synchronize()
+    return host_out
+
+
 def run_chain(wave: Wave, stages, backend: str = "auto", strategy: str = "auto") -> Wave:
     """Record bound ``stages`` on ``wave``; custom stages run eagerly."""
     if not isinstance(wave, Wave):

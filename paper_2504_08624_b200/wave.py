@@ -190,9 +190,32 @@ class Wave:
             return self._dev.to(device)
         return self._dev
 
+    def _host_streamable(self) -> bool:
+        """A pending chain over a host-resident (pinned) source: its result can
+        be streamed host -> device -> host in channel blocks."""
+        src = self._src
+        return (self._entries is not None and src is not None and src._dev is None and src._entries is None
+                and src._pinned is not None)
+
     def numpy32(self, out=None) -> np.ndarray:
         """Float32 host copy (``out`` may be a preallocated, e.g. pinned, array
-        or tensor to copy into)."""
+        or tensor to copy into). A chain over a pinned host source is streamed:
+        uploads, the fused passes and downloads of channel blocks overlap."""
+        torch = _torch()
+        if self._host_streamable() and (out is None or (isinstance(out, torch.Tensor) and out.is_pinned())):
+            from . import engine
+
+            dst = out if out is not None else torch.empty(self._shape, dtype=torch.float32, pin_memory=True)
+            engine.stream_host_entries(self._entries, self._src._pinned, dst)
+            if out is not None:
+                return out
+            host = dst.numpy()
+            host.setflags(write=False)
+            object.__setattr__(self, "_host32", host)
+            object.__setattr__(self, "_pinned", dst)
+            object.__setattr__(self, "_src", None)
+            object.__setattr__(self, "_entries", None)
+            return host
         self._materialize()
         if out is not None:
             torch = _torch()

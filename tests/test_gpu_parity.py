@@ -336,3 +336,28 @@ def test_plan_uses_intended_kernel(stages, fs, kernel):
     plan = engine.plan_for(wp.Chain(stages()).bind(fs).stages, device=0)
     desc = plan.describe()
     assert len(desc) == 1 and desc[0].startswith(kernel), desc
+
+
+# ---- host -> device -> host streaming (pinned sources, channel blocks) -------
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C", [1, 5, 32])
+@pytest.mark.parametrize("fir_taps", [101, 2048])
+def test_streamed_host_path_bit_exact(C, fir_taps):
+    import torch
+
+    fs = 48000
+    w = wp.white_noise(0.25, C, fs, seed=21)
+    chain = wp.Chain([wp.design_butterworth("hp", 4, 100), wp.design_fir("lp", fir_taps, 4000), wp.Gain(0.5)]) \
+        if fir_taps <= 129 else wp.Chain([wp.design_fir("lp", fir_taps, 4000)])
+    ref = (w | chain).numpy32().copy()
+    pinned = torch.empty((C, w.frames), dtype=torch.float32, pin_memory=True)
+    pinned.copy_(w.tensor())
+    src = wp.Wave.from_tensor(pinned, fs)
+    out = torch.empty_like(pinned).pin_memory()
+    lazy = src | chain
+    assert lazy._host_streamable()
+    lazy.numpy32(out=out)
+    assert np.array_equal(out.numpy(), ref)
+    assert np.array_equal((src | chain).numpy32(), ref)  # pinned result allocated internally
