@@ -20,6 +20,8 @@ one channel, validation errors, exact ``==`` and ``hash``.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from .errors import InvalidArgument
@@ -184,7 +186,9 @@ class Wave:
             if self._pinned is not None:
                 host = self._pinned
             else:
-                host = torch.from_numpy(np.ascontiguousarray(self._host32))
+                with warnings.catch_warnings():  # read-only array: only copied to the device
+                    warnings.simplefilter("ignore", UserWarning)
+                    host = torch.from_numpy(np.ascontiguousarray(self._host32))
             object.__setattr__(self, "_dev", host.to(dev, non_blocking=True))
         if device is not None and self._dev.device != torch.device(device):
             return self._dev.to(device)

@@ -361,3 +361,65 @@ def test_streamed_host_path_bit_exact(C, fir_taps):
     lazy.numpy32(out=out)
     assert np.array_equal(out.numpy(), ref)
     assert np.array_equal((src | chain).numpy32(), ref)  # pinned result allocated internally
+
+
+# ---- FFT overlap-save path: ragged lengths, odd channel counts ---------------
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_taps", [513, 2048, 4096])
+@pytest.mark.parametrize("frames", [1, 100, 4095, 12288, 12289, 30001])
+def test_fft_path_ragged_vs_oracle(n_taps, frames):
+    rng = np.random.default_rng(n_taps + frames)
+    taps = rng.standard_normal(n_taps) / np.sqrt(n_taps)
+    for C in (1, 3):
+        x = rng.standard_normal((C, frames)).astype(np.float32).astype(np.float64)
+        y = wp.apply_fir(wp.FirFilter.from_taps(taps, 48000), wp.Wave(x, 48000), strategy="fft").samples
+        assert oracle.parity_error(y, oracle.fir_direct(taps, x)) <= FIR_TOL, (C, frames)
+
+
+# ---- C ABI with padded, unaligned row strides --------------------------------
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chain_kind", ["cfg3", "fir101", "fir4096", "lp8"])
+def test_plan_execute_unaligned_strides(chain_kind):
+    import torch
+
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    stages = {
+        "cfg3": _cfg3(),
+        "fir101": [wp.design_fir("lp", 101, 1000)],
+        "fir4096": [wp.design_fir("lp", 4096, 2000)],
+        "lp8": [wp.design_butterworth("lp", 8, 2000)],
+    }[chain_kind]
+    bound = wp.Chain(stages).bind(fs).stages
+    C, N = 3, 30011
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal((C, N)).astype(np.float32)
+    ldx, ldy = N + 3, N + 5  # rows not 16-byte aligned: scalar edge paths
+    xd = torch.zeros((C, ldx), dtype=torch.float32, device="cuda")
+    xd[:, :N] = torch.from_numpy(x)
+    yd = torch.full((C, ldy), 7.0, dtype=torch.float32, device="cuda")
+    plan = engine.plan_for(bound, device=0)
+    nb = plan.workspace_bytes(C, N)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    plan.execute(xd.data_ptr(), yd.data_ptr(), C, N, ldx, ldy, ws.data_ptr(), nb, torch.cuda.current_stream().cuda_stream)
+    got = yd.cpu().numpy()
+    assert np.all(got[:, N:] == 7.0)  # padding untouched
+    ref = oracle.pipe(x.astype(np.float64), bound)
+    tol = FIR_TOL if chain_kind.startswith("fir") else IIR_TOL
+    assert oracle.parity_error(got[:, :N].astype(np.float64), ref) <= tol
+
+
+@pytest.mark.gpu
+def test_many_channels_lp8_subset_parity():
+    fs = 48000
+    w = wp.white_noise(0.4, 300, fs, seed=33)
+    lp8 = wp.design_butterworth("lp", 8, 2000)
+    y = (w | lp8).samples
+    for c in (0, 1, 150, 299):
+        ref = oracle.pipe(w.samples[c:c + 1], [lp8.bind(fs)])
+        assert oracle.parity_error(y[c:c + 1], ref) <= IIR_TOL, c
