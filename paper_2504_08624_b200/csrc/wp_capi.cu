@@ -279,6 +279,11 @@ bool chain_tc_enabled() {
     return !(v && std::string(v) == "cuda");
 }
 
+bool chain_tc_forced() {
+    const char *v = std::getenv("WP_CHAIN_IMPL");
+    return v && std::string(v) == "tc";
+}
+
 // Build the tensor-core chain tables of pass p: combined response g (Toeplitz
 // B image, fp16 hi/lo), state-term matrix E, chunk-scan tables (M = A^64).
 int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
@@ -490,7 +495,11 @@ int finalize_pass(Pass &p) {
         p.tc_W = wpk::TC_N * (wpk::TC_M - 1) + p.tc_K;
         p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
     }
-    if (p.S > 0 && chain_tc_enabled()) {
+    // IIR + FIR passes run on the tensor-core chain kernel; IIR-only passes stay
+    // on the CUDA-core chunked scan, which measured faster for them (cfg5
+    // slice 295 vs 254 G ch-s/s, cfg3's IIR part 0.97 vs 1.25 ms;
+    // tools/iir_probe.py). WP_CHAIN_IMPL=tc forces the tensor-core kernel.
+    if (p.S > 0 && chain_tc_enabled() && (p.T > 1 || chain_tc_forced())) {
         const int T = p.T > 0 ? p.T : 1;
         const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
         const int K = H + 64;

@@ -151,7 +151,9 @@ struct SmemLayout {
     static constexpr size_t region_bytes = sizeof(float) * REGION;
     static constexpr size_t g = region + region_bytes;
     static constexpr size_t g_bytes = S > 0 ? sizeof(TS) * D * D * 33 : 0;
-    static constexpr size_t misc = (g + g_bytes + 15) & ~size_t(15);
+    static constexpr size_t tp = (g + g_bytes + 15) & ~size_t(15);
+    static constexpr size_t tp_bytes = S > 0 ? sizeof(TS) * 33 * D * D : 0;  // look-back powers (M^T)^j
+    static constexpr size_t misc = (tp + tp_bytes + 15) & ~size_t(15);
     // warp_incl[NW][D], wc[NW][D], WC[NW][D], agg[D], sin[D], agg_incl[D]
     static constexpr size_t misc_bytes = sizeof(TS) * (3 * NW * D + 3 * D) + 16;
     static constexpr size_t taps = (misc + misc_bytes + 15) & ~size_t(15);
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
     float *region = reinterpret_cast<float *>(smem + Lay::region);
     float4 *reg4 = reinterpret_cast<float4 *>(region);
     TS *gsm = reinterpret_cast<TS *>(smem + Lay::g);
+    TS *tpsm = reinterpret_cast<TS *>(smem + Lay::tp);
     long long *tile_s = reinterpret_cast<long long *>(smem + Lay::misc);
     TS *warp_incl = reinterpret_cast<TS *>(smem + Lay::misc + 16);
     TS *wc_s = warp_incl + NW * D;
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
     if constexpr (S > 0) {
         const TS *G = reinterpret_cast<const TS *>(a.G);
         for (int i = tid; i < D * D * 33; i += NT) gsm[i] = G[i];
+        const TS *TPg = reinterpret_cast<const TS *>(a.TP);
+        for (int i = tid; i < 33 * D * D; i += NT) tpsm[i] = TPg[i];
     }
     if constexpr (FIR) {
         for (int i = tid; i < a.Tpad; i += NT) taps_s[i] = a.taps[i];
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
             if (warp == 0) {
                 TileRec<TS, D> *recs = reinterpret_cast<TileRec<TS, D> *>(a.recs);
                 TileRec<TS, D> *mine = recs + tile;
-                const TS *TP = reinterpret_cast<const TS *>(a.TP);
+                const TS *TP = tpsm;  // staged in shared memory: one L2 round trip less per look-back
                 TS agg[D], carry[D];
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
 #pragma unroll
                     for (int i = 0; i < D; ++i) val[i] = ldcg(sv + i);
                     const TS *Mj = TP + (size_t)pw * D * D;
-                    matvec_acc<D, TS>(carry, val, [&](int i, int j) { return ldcg(Mj + i * D + j); });
+                    matvec_acc<D, TS>(carry, val, [&](int i, int j) { return Mj[i * D + j]; });
                 }
 #pragma unroll
                 for (int i = 0; i < D; ++i) {

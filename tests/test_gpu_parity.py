@@ -324,8 +324,8 @@ def test_fir_tensor_core_zeros_and_tail():
     [
         (lambda: [wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
                   wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, "chain_tc"),   # cfg3
-        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, "chain_tc"),              # cfg5
-        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, "chain_tc"),              # cfg1
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, "fused"),                 # cfg5
+        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, "fused"),                 # cfg1
         (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, "fir_tc"),            # cfg2
         (lambda: [wp.design_fir("lp", 4096, 2000, "hamming")], 48000, "fft_ols"),          # cfg4
     ],
