@@ -115,6 +115,20 @@ int wp_white_noise(float *y, int64_t channels, int64_t frames, int64_t ld_y, uin
 int wp_peak_abs(const float *x, int64_t channels, int64_t frames, int64_t ld_x, float *out_device,
                 wp_stream_t stream);
 
+/* ---- WAV payload codec (wavio.py:49-200), device side ----
+ * The RIFF header is parsed/written by the host; these convert the data
+ * chunk. payload: DEVICE pointer to the little-endian interleaved frames
+ * (channels x frames samples); y / x: planar float32 [channels][ld].
+ * Decode is exact (pcm16 / 2^15, pcm24 / 2^23, float32 bit copy); encode
+ * clamps to [-1, 1] and quantizes round-half-away-from-zero like
+ * wavio.save_wav, counting |x| > 1 samples into *clipped_device (uint64,
+ * zeroed by the call; may be NULL for float32). */
+enum { WP_ENC_PCM16 = 16, WP_ENC_PCM24 = 24, WP_ENC_F32 = 32 };
+int wp_wav_decode(const void *payload, int32_t encoding, float *y, int64_t channels, int64_t frames, int64_t ld_y,
+                  wp_stream_t stream);
+int wp_wav_encode(const float *x, int64_t channels, int64_t frames, int64_t ld_x, int32_t encoding, void *payload,
+                  uint64_t *clipped_device, wp_stream_t stream);
+
 /* ---- diagnostics ---- */
 const char *wp_last_error(void);
 int wp_abi_version(void);

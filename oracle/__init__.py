@@ -21,6 +21,9 @@ Contents (each restates the reference path, citations into /root/reference):
 * ``save_wav_float32`` / ``load_wav``: the float32 WAV path of wavio.py:49-114,
   only to reproduce the reference's end-to-end golden sha256
   (tests/golden/golden_hashes.json, test_acceptance.py:203-245).
+* ``wav_encode`` / ``wav_decode`` / ``wav_file_bytes``: pcm16/pcm24/float32
+  payload restatement of wavio.py:69-98 and :193-200 (checker of the device
+  WAV codec; pinned by tests/golden/wav_golden.json from the reference).
 """
 
 from __future__ import annotations
@@ -271,6 +274,54 @@ def load_wav_float32(path: str):
         off += 8 + size + (size & 1)
     inter = np.frombuffer(data, dtype="<f4").astype(np.float64)
     return np.ascontiguousarray(inter.reshape(-1, channels).T), fs
+
+
+# --- WAV payloads (wavio.py:69-98 encode, :193-200 decode) ------------------
+
+_WAV_BITS = {"pcm16": 16, "pcm24": 24, "float32": 32}
+
+
+def wav_encode(samples, encoding: str):
+    """Interleaved little-endian payload bytes and the clipped-sample count
+    of planar ``samples`` (save_wav, wavio.py:69-98)."""
+    inter = np.ascontiguousarray(_planar(samples).T)
+    if encoding == "float32":
+        return inter.astype(np.float32).tobytes(), 0
+    bits = _WAV_BITS[encoding]
+    clipped = int(np.count_nonzero(np.abs(inter) > 1.0))
+    full = float(2 ** (bits - 1))
+    c = np.clip(inter, -1.0, 1.0)
+    q = np.clip(np.copysign(np.floor(np.abs(c) * full + 0.5), c), -full, full - 1).astype(np.int32)
+    if bits == 16:
+        return q.astype("<i2").tobytes(), clipped
+    b4 = np.frombuffer(q.astype("<i4").tobytes(), dtype=np.uint8).reshape(-1, 4)
+    return np.ascontiguousarray(b4[:, :3]).tobytes(), clipped
+
+
+def wav_decode(payload: bytes, encoding: str, channels: int) -> np.ndarray:
+    """Planar float64 samples of an interleaved payload (wavio.py:193-200)."""
+    if encoding == "pcm16":
+        v = np.frombuffer(payload, dtype="<i2").astype(np.float64) / 2.0**15
+    elif encoding == "pcm24":
+        t = np.frombuffer(payload, dtype=np.uint8).reshape(-1, 3).astype(np.int32)
+        v = (((t[:, 0] << 8) | (t[:, 1] << 16) | (t[:, 2] << 24)) >> 8).astype(np.float64) / 2.0**23
+    else:
+        v = np.frombuffer(payload, dtype="<f4").astype(np.float64)
+    return np.ascontiguousarray(v.reshape(-1, channels).T)
+
+
+def wav_file_bytes(samples, fs: int, encoding: str):
+    """Canonical RIFF/WAVE file bytes (fmt + data chunk) and clipped count."""
+    samples = _planar(samples)
+    payload, clipped = wav_encode(samples, encoding)
+    bits = _WAV_BITS[encoding]
+    tag = 3 if encoding == "float32" else 1
+    channels = samples.shape[0]
+    block = channels * bits // 8
+    fmt = struct.pack("<4sIHHIIHH", b"fmt ", 16, tag, channels, fs, fs * block, block, bits)
+    pad = b"\x00" if len(payload) % 2 else b""
+    data = struct.pack("<4sI", b"data", len(payload)) + payload + pad
+    return struct.pack("<4sI4s", b"RIFF", 4 + len(fmt) + len(data), b"WAVE") + fmt + data, clipped
 
 
 def parity_error(y, y_ref) -> float:

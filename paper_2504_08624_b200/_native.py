@@ -34,6 +34,8 @@ WP_IIR_PREC_F64 = 32
 EXPORTED = (
     "wp_plan_create",
     "wp_set_trace",
+    "wp_wav_decode",
+    "wp_wav_encode",
     "wp_plan_destroy",
     "wp_plan_workspace_bytes",
     "wp_plan_execute",
@@ -99,9 +101,12 @@ def load(require_device: bool = False):
             lib.wp_last_error.restype = ctypes.c_char_p
             lib.wp_launch_count.restype = ctypes.c_uint64
             lib.wp_set_trace.argtypes = [vp, sz]
+            lib.wp_wav_decode.argtypes = [vp, i32, vp, i64, i64, i64, vp]
+            lib.wp_wav_encode.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp]
             for name in ("wp_plan_create", "wp_plan_destroy", "wp_plan_workspace_bytes", "wp_plan_execute",
                          "wp_plan_num_passes", "wp_plan_launches", "wp_iir_cascade", "wp_fir",
-                         "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace"):
+                         "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace",
+                         "wp_wav_decode", "wp_wav_encode"):
                 getattr(lib, name).restype = ctypes.c_int
             _lib = lib
     if require_device:
@@ -125,6 +130,16 @@ def check(rc: int, what: str = "") -> None:
 def check_device() -> None:
     lib = load(require_device=True)
     check(lib.wp_check_device(), "device check")
+
+
+def wav_decode(payload_ptr: int, encoding: int, y_ptr: int, channels: int, frames: int, ld: int, stream: int) -> None:
+    check(load(require_device=True).wp_wav_decode(payload_ptr, encoding, y_ptr, channels, frames, ld, stream), "wav decode")
+
+
+def wav_encode(x_ptr: int, channels: int, frames: int, ld: int, encoding: int, payload_ptr: int, clipped_ptr,
+               stream: int) -> None:
+    check(load(require_device=True).wp_wav_encode(x_ptr, channels, frames, ld, encoding, payload_ptr, clipped_ptr, stream),
+          "wav encode")
 
 
 def set_trace(ptr: int, entries: int) -> None:

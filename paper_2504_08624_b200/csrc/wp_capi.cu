@@ -1029,6 +1029,35 @@ int wp_white_noise(float *y, int64_t channels, int64_t frames, int64_t ld_y, uin
     return e == cudaSuccess ? WP_OK : cuda_fail(e, "white_noise launch");
 }
 
+int wp_wav_decode(const void *payload, int32_t encoding, float *y, int64_t channels, int64_t frames, int64_t ld_y,
+                  wp_stream_t stream) {
+    if (!payload || !y || channels < 1 || frames < 1 || ld_y < frames) return fail(WP_EINVAL, "bad wav decode arguments");
+    if (encoding != WP_ENC_PCM16 && encoding != WP_ENC_PCM24 && encoding != WP_ENC_F32)
+        return fail(WP_EINVAL, "encoding must be 16 (pcm16), 24 (pcm24) or 32 (float32)");
+    int rc = arch_ok();
+    if (rc != WP_OK) return rc;
+    cudaError_t e = wp::launch_wav_decode(payload, encoding, y, channels, frames, ld_y, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? WP_OK : cuda_fail(e, "wav decode launch");
+}
+
+int wp_wav_encode(const float *x, int64_t channels, int64_t frames, int64_t ld_x, int32_t encoding, void *payload,
+                  uint64_t *clipped_device, wp_stream_t stream) {
+    if (!x || !payload || channels < 1 || frames < 1 || ld_x < frames) return fail(WP_EINVAL, "bad wav encode arguments");
+    if (encoding != WP_ENC_PCM16 && encoding != WP_ENC_PCM24 && encoding != WP_ENC_F32)
+        return fail(WP_EINVAL, "encoding must be 16 (pcm16), 24 (pcm24) or 32 (float32)");
+    if (encoding != WP_ENC_F32 && !clipped_device) return fail(WP_EINVAL, "pcm encodings need a clipped-count buffer");
+    int rc = arch_ok();
+    if (rc != WP_OK) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (clipped_device) {
+        cudaError_t e0 = cudaMemsetAsync(clipped_device, 0, sizeof(uint64_t), s);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "memset(clipped)");
+    }
+    cudaError_t e = wp::launch_wav_encode(x, channels, frames, ld_x, encoding, payload,
+                                          reinterpret_cast<unsigned long long *>(clipped_device), s);
+    return e == cudaSuccess ? WP_OK : cuda_fail(e, "wav encode launch");
+}
+
 int wp_peak_abs(const float *x, int64_t channels, int64_t frames, int64_t ld_x, float *out_device, wp_stream_t stream) {
     if (!x || !out_device || channels < 1 || frames < 1 || ld_x < frames) return fail(WP_EINVAL, "bad peak arguments");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -89,6 +89,12 @@ size_t chain_tc_smem_bytes(int W, int K, int S, bool f64);
 cudaError_t launch_chain_tc(bool f64, int S, const wpk::ChainTcArgs &a, const HostTables &t,
                             const std::vector<double> &E, int grid, size_t smem, cudaStream_t st);
 
+// WAV payload codec (wp_wav.cu)
+cudaError_t launch_wav_decode(const void *payload, int enc, float *y, long long C, long long N, long long ld,
+                              cudaStream_t st);
+cudaError_t launch_wav_encode(const float *x, long long C, long long N, long long ld, int enc, void *payload,
+                              unsigned long long *clipped, cudaStream_t st);
+
 // FFT overlap-save long FIR (wp_fft_ols.cu)
 size_t fft_ols_smem_bytes();
 cudaError_t launch_fft_ols(const wpk::FftArgs &a, int grid, cudaStream_t st);
