@@ -237,6 +237,10 @@ struct Pass {
     std::vector<double> ct_E;  // [64][D]
     unsigned char *d_Bk = nullptr;  // int8 digit planes of the chunk-state weights
     double ct_kscale[8] = {0};
+    // decoupled tensor-core chain (rows -> carry -> gemm kernels)
+    bool chain3 = false;
+    unsigned char *d_Eimg = nullptr;  // tf32 parts of the state-term matrix E
+    double c3_st_scale = 1.0;
     std::string desc;
     bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
 };
@@ -281,7 +285,23 @@ bool chain_tc_enabled() {
 
 bool chain_tc_forced() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
-    return v && std::string(v) == "tc";
+    return v && (std::string(v) == "tc" || std::string(v) == "tc1");
+}
+
+// WP_CHAIN_IMPL=tc1 selects the single-kernel look-back chain (wp_chain_tc.cuh)
+// instead of the decoupled three-kernel chain (wp_chain3.cuh).
+bool chain_single_kernel() {
+    const char *v = std::getenv("WP_CHAIN_IMPL");
+    return v && std::string(v) == "tc1";
+}
+
+float tf32_round(double v) {
+    float f = (float)v;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u = (u + 0x1000u) & 0xFFFFE000u;
+    std::memcpy(&f, &u, 4);
+    return f;
 }
 
 // Build the tensor-core chain tables of pass p: combined response g (Toeplitz
@@ -345,10 +365,19 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
             const float val = (t >= 0 && t < K) ? (float)std::ldexp(g[t], fB) : 0.f;
             const __half hi = __float2half_rn(val);
             const __half lo = __float2half_rn(val - __half2float(hi));  // unscaled: one accumulator
-            const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
-            const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
-            img[phys / 2] = hi;
-            img[split + phys / 2] = lo;
+            if (chain_single_kernel()) {
+                // [part][atom][64 rows][128 B]
+                const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
+                const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
+                img[phys / 2] = hi;
+                img[split + phys / 2] = lo;
+            } else {
+                // [atom][hi rows 0..63 | lo rows 64..127][128 B]: one N = 128 operand per K atom
+                const uint32_t logical = (uint32_t)(k / 64) * 16384u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
+                const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
+                img[phys / 2] = hi;
+                img[(phys + 8192u) / 2] = lo;
+            }
         }
     cudaError_t e = cudaMalloc(&p.d_Bimg, img.size() * sizeof(__half));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");
@@ -402,6 +431,31 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
     e = cudaMemcpy(p.d_TP, tbuf.data(), tbuf.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(TP)");
     p.chain_tc = true;
+    if (!chain_single_kernel()) {
+        // state-term operand of chain_gemm: E[p][d] x 2^fB in three tf32 parts,
+        // no-swizzle K-major rows of 8 states (32 B), zero for d >= D
+        std::vector<float> eimg(3 * 512, 0.f);
+        for (int q = 0; q < 64; ++q)
+            for (int i = 0; i < D; ++i) {
+                const double v = p.ct_E[q * D + i];
+                const float t1 = tf32_round(v);
+                const double r1 = v - (double)t1;
+                const float t2 = tf32_round(r1);
+                const float t3 = tf32_round(r1 - (double)t2);
+                const uint32_t o = wpk::c3d::off32(q, i) / 4;
+                eimg[o] = t1;
+                eimg[512 + o] = t2;
+                eimg[1024 + o] = t3;
+            }
+        cudaError_t e3 = cudaMalloc(&p.d_Eimg, eimg.size() * sizeof(float));
+        if (e3 != cudaSuccess) return cuda_fail(e3, "cudaMalloc(Eimg)");
+        e3 = cudaMemcpy(p.d_Eimg, eimg.data(), eimg.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e3 != cudaSuccess) return cuda_fail(e3, "cudaMemcpy(Eimg)");
+        p.c3_st_scale = std::ldexp(1.0, fB);
+        p.chain3 = true;
+        p.chain_tc = false;
+        smem = wp::chain3_smem_bytes(W, K, S, f64);
+    }
     p.f64 = f64;
     p.ct_H = H;
     p.ct_K = K;
@@ -410,9 +464,15 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
     p.grid_cap = wp::sm_count();
     p.Lout = wpk::CT_TOUT;
     char buf[256];
-    snprintf(buf, sizeof buf,
-             "chain_tc[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3 M128xN64 K=%d halo=%d tile=%d smem=%zu",
-             (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
+    if (p.chain3)
+        snprintf(buf, sizeof buf,
+                 "chain_rows+chain_carry+chain_gemm[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3+tf32x6 M128xN64 "
+                 "K=%d halo=%d tile=%d smem=%zu",
+                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
+    else
+        snprintf(buf, sizeof buf,
+                 "chain_tc[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3 M128xN64 K=%d halo=%d tile=%d smem=%zu",
+                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
     p.desc = buf;
     return WP_OK;
 }
@@ -508,7 +568,8 @@ int finalize_pass(Pass &p) {
         double rmax = 0;
         for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
         const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
-        const size_t smem = wp::chain_tc_smem_bytes(W, K, p.S, f64);
+        const size_t smem = chain_single_kernel() ? wp::chain_tc_smem_bytes(W, K, p.S, f64)
+                                                  : wp::chain3_smem_bytes(W, K, p.S, f64);
         if (W / 4 <= wpk::CT_QMAX * wpk::CT_CONV && smem <= 227 * 1024) {
             int rc = build_chain_tc(p, H, K, W, f64, smem);
             if (rc != WP_OK) return rc;
@@ -622,6 +683,8 @@ void free_pass(Pass &p) {
     p.d_Bimg = nullptr;
     if (p.d_Bk) cudaFree(p.d_Bk);
     p.d_Bk = nullptr;
+    if (p.d_Eimg) cudaFree(p.d_Eimg);
+    p.d_Eimg = nullptr;
     if (p.d_H) cudaFree(p.d_H);
     if (p.d_tw) cudaFree(p.d_tw);
     p.d_H = p.d_tw = nullptr;
@@ -635,6 +698,7 @@ void free_pass(Pass &p) {
 size_t rec_bytes(const Pass &p) {
     if (p.kind != Pass::FUSED || p.S == 0) return 0;
     const size_t es = p.f64 ? 8 : 4;
+    if (p.chain3) return (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 8);  // row prefixes, segment aggregates + carries
     return (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
 }
 
@@ -795,7 +859,7 @@ int wp_plan_num_passes(const wp_plan *plan) { return plan ? (int)plan->passes.si
 int wp_plan_launches(const wp_plan *plan) {
     if (!plan) return 0;
     int n = 0;
-    for (const Pass &p : plan->passes) n += p.kind == Pass::FUSED ? 1 : 2;
+    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : p.chain3 ? 3 : 1;
     return n;
 }
 
@@ -880,6 +944,66 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             const int grid = (int)std::min<long long>(a.total, p.grid_cap);
             e = wp::launch_fft_ols(a, grid, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
+        } else if (p.chain3) {
+            wp::Chain3Launch L;
+            const long long T = (N + wpk::CT_TOUT - 1) / wpk::CT_TOUT;
+            const long long tiles = T * C;
+            if (tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
+            const int D = 2 * p.S;
+            const size_t es = p.f64 ? 8 : 4;
+            unsigned char *rows = ws + rec_off;
+            unsigned char *aggs = rows + (size_t)tiles * wpk::CT_ROWS * D * es;
+            unsigned char *carry = aggs + (size_t)tiles * 4 * D * es;
+            const int vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+            const int vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+            L.rows = wpk::C3RowsArgs{in, C, N, ld_in, tiles, p.ct_H, vec_x, p.d_G, rows, aggs};
+            const long long segs = 4 * T;
+            const int B = (int)((segs + wpk::C3_CARRY_THREADS - 1) / wpk::C3_CARRY_THREADS);
+            L.carry = wpk::C3CarryArgs{C, segs, B, aggs, carry};
+            {
+                // segment transfer M^32 = W[1]; thread-block and warp powers
+                const Mat MT(p.tables.W.begin() + (size_t)D * D, p.tables.W.begin() + (size_t)2 * D * D);
+                const Mat MB = matpow(MT, B, D);
+                L.carry_mats.assign((size_t)7 * D * D, 0.0);
+                std::copy(MT.begin(), MT.end(), L.carry_mats.begin());
+                Mat q = MB;
+                for (int i = 0; i < 5; ++i) {
+                    std::copy(q.begin(), q.end(), L.carry_mats.begin() + (size_t)(1 + i) * D * D);
+                    q = matmul(q, q, D);
+                }
+                const Mat R = matpow(MB, 32, D);
+                std::copy(R.begin(), R.end(), L.carry_mats.begin() + (size_t)6 * D * D);
+            }
+            wpk::C3GemmArgs &g = L.gemm;
+            g = wpk::C3GemmArgs{};
+            g.x = in;
+            g.y = out;
+            g.C = C;
+            g.N = N;
+            g.ldx = ld_in;
+            g.ldy = ld_out;
+            g.total_tiles = tiles;
+            g.H = p.ct_H;
+            g.K = p.ct_K;
+            g.W = p.ct_W;
+            g.Bimg = p.d_Bimg;
+            g.Eimg = p.d_Eimg;
+            g.out_scale = p.ct_out_scale;
+            g.st_scale = p.c3_st_scale;
+            g.G = p.d_G;
+            g.rows = rows;
+            g.carry = carry;
+            g.vec_x = vec_x;
+            g.vec_y = vec_y;
+            {
+                const char *dv = std::getenv("WP_CT_DBG");
+                g.dbg = dv ? std::atoi(dv) : 0;
+            }
+            g.trace = (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV) ? g_trace : nullptr;
+            L.gemm_grid = (int)std::min<long long>(tiles, p.grid_cap);
+            L.smem = p.smem;
+            e = wp::launch_chain3(p.f64, p.S, L, p.tables, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "chain3 launch");
         } else if (p.chain_tc) {
             wpk::ChainTcArgs a{};
             a.x = in;

@@ -1,0 +1,85 @@
+// Instantiations and launchers of the decoupled tensor-core chain
+// (wp_chain3.cuh): scan dtype float64 or float32, 1..4 SOS sections.
+#include <algorithm>
+
+#include "wp_chain3.cuh"
+#include "wp_internal.h"
+
+namespace wp {
+
+namespace {
+
+template <typename TS, int S>
+wpk::C3RowsTables<TS, 2 * S> c3_rows_tables(const HostTables &t) {
+    constexpr int D = 2 * S;
+    wpk::C3RowsTables<TS, D> tb{};
+    for (int n = 0; n < 64; ++n)
+        for (int i = 0; i < D; ++i) tb.K[n][i] = TS(t.K[n * D + i]);
+    for (int q = 0; q < 5; ++q)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) tb.P[q][i][j] = TS(t.P[(q * D + i) * D + j]);
+    for (int w = 0; w < 4; ++w)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) tb.W[w][i][j] = TS(t.W[(w * D + i) * D + j]);
+    return tb;
+}
+
+template <typename TS, int S>
+cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream_t st) {
+    constexpr int D = 2 * S;
+    const wpk::C3RowsTables<TS, D> tb = c3_rows_tables<TS, S>(t);
+    // chain_rows: persistent, as many CTAs as fit
+    static int rows_occ = 0;
+    if (!rows_occ) {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>,
+                                                                      wpk::C3_ROWS_THREADS, 0);
+        if (e != cudaSuccess) return e;
+        rows_occ = std::max(occ, 1);
+    }
+    const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ * sm_count());
+    wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, 0, st>>>(L.rows, tb);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // chain_carry: one CTA per channel
+    wpk::C3CarryTables<TS, D> ct{};
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            ct.MT[i][j] = TS(L.carry_mats[i * D + j]);
+            for (int q = 0; q < 5; ++q) ct.Q[q][i][j] = TS(L.carry_mats[((1 + q) * D + i) * D + j]);
+            ct.R[i][j] = TS(L.carry_mats[(6 * D + i) * D + j]);
+        }
+    wpk::chain_carry_kernel<TS, S><<<(unsigned)L.carry.C, wpk::C3_CARRY_THREADS, 0, st>>>(L.carry, ct);
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // chain_gemm: one CTA per SM
+    auto kern = wpk::chain_gemm_kernel<TS, S>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename TS>
+cudaError_t c3_dispatch(int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st) {
+    switch (S) {
+        case 1: return c3_launch_one<TS, 1>(L, t, st);
+        case 2: return c3_launch_one<TS, 2>(L, t, st);
+        case 3: return c3_launch_one<TS, 3>(L, t, st);
+        case 4: return c3_launch_one<TS, 4>(L, t, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+size_t chain3_smem_bytes(int W, int K, int S, bool f64) { return wpk::C3Layout(W, K, 2 * S, f64 ? 8 : 4).total; }
+
+cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st) {
+    return f64 ? c3_dispatch<double>(S, L, t, st) : c3_dispatch<float>(S, L, t, st);
+}
+
+}  // namespace wp

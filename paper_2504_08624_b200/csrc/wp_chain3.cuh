@@ -1,0 +1,795 @@
+// Decoupled tensor-core chain for sm_100a: pre-gain -> IIR SOS cascade -> FIR
+// -> post-gains as three kernels with NO serial dependency between tiles
+// inside any of them.
+//
+// Replaces the reference's per-stage passes (_iir_channel, _kernels_jit.py:
+// 14-32; _fir_channel, :51-62; Chain.apply's stage loop, chain.py:66-71).
+//
+// Same LTI formulation as wp_chain_tc.cuh: for tile rows
+// m = 0..127 of 64 outputs (n = n0 + 64 m + p), window start w_m = n0 - H + 64 m,
+//
+//   y[n] = sum_{k < H+64} g[p + H - k] x[w_m + k]  +  sum_i E[p][i] s_{w_m}[i]
+//   s_{w_{m+1}} = M s_{w_m} + e_m,   e_m = sum_j A^(63-j) B x[w_m + j],  M = A^64
+//
+// The single-kernel version chains tiles through a decoupled look-back, so a
+// tile's output waits on the aggregates of tiles other SMs are processing at
+// the same moment; the whole pipeline then runs at the latency of that chain.
+// Here the recurrence is split along its data dependencies:
+//
+//   chain_rows   (CUDA cores, every tile independent)  e_m in TS from the fp32
+//                samples, Kogge-Stone row scan, zero-carry row prefixes L_m
+//                -> HBM (D TS per row), tile aggregate -> HBM
+//   chain_carry  (one CTA per channel, tiny)  carry_k = state entering tile k:
+//                blocked scan over the channel's tile aggregates
+//   chain_gemm   (tensor cores, every tile independent)  main GEMM fp16 x3 into
+//                TMEM, then the state term as a tf32 GEMM into the SAME
+//                accumulator: s_m = L_m + M^m carry_k split into three tf32
+//                parts x E split into three tf32 parts (6 MMAs, K = 8), so the
+//                epilogue is TMEM -> scale -> store.
+//
+// Extra HBM traffic: the samples are read twice and the row prefixes
+// (D * sizeof(TS) / 64 bytes per sample) are written once and read once.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "wp_chain_tc.cuh"
+
+namespace wpk {
+
+constexpr int C3_THREADS = 512;
+constexpr int C3_NA = 4;          // TMEM accumulator stages (64 columns each)
+constexpr int C3_ROWS_THREADS = 128;
+constexpr int C3_CARRY_THREADS = 256;
+
+struct C3RowsArgs {
+    const float *x;
+    long long C, N, ldx;
+    long long total_tiles;
+    int H;
+    int vec_x;
+    const void *G;  // [D][D][33] TS, M^l lane-minor
+    void *rows;     // [tiles][128][D] TS: zero-carry prefixes within each 32-row segment
+    void *aggs;     // [tiles][4][D] TS: segment aggregates
+};
+
+template <typename TS, int D>
+struct C3RowsTables {
+    TS K[64][D];     // A^(63-j) B
+    TS P[5][D][D];   // M^(2^i)
+    TS W[4][D][D];   // M^(32 w)
+};
+
+struct C3CarryArgs {
+    long long C, T;  // channels, segments per channel (4 per tile)
+    int B;           // segments per thread
+    const void *aggs;
+    void *carry;     // [tiles][4][D] TS: state entering each segment
+};
+
+template <typename TS, int D>
+struct C3CarryTables {
+    TS MT[D][D];     // M^32: one segment
+    TS Q[5][D][D];   // MT^(B 2^i)
+    TS R[D][D];      // MT^(32 B): one warp of threads
+};
+
+struct C3GemmArgs {
+    const float *x;
+    float *y;
+    long long C, N, ldx, ldy;
+    long long total_tiles;
+    int H, K, W;
+    const unsigned char *Bimg;  // [2][atoms][64 rows][128 B] SW128 K-major fp16 hi / lo of g
+    const unsigned char *Eimg;  // [3][64 rows][8] tf32 parts of E, no-swizzle K-major, 32-B rows
+    float out_scale;            // 2^-fB of the g image
+    double st_scale;            // 2^fB: state operand s' = s * sc * st_scale
+    const void *G;              // [D][D][33] TS
+    const void *rows;           // [tiles][128][D] TS
+    const void *carry;          // [tiles][4][D] TS
+    int vec_x, vec_y;
+    int dbg;                    // 4 = no state term
+    unsigned long long *trace;  // optional: [tiles][C3_TRACE_EV] globaltimer stamps
+};
+constexpr int C3_TRACE_EV = 8;
+
+namespace c3d {
+
+// no-swizzle K-major, 32-byte rows: core matrices of 8 rows x 16 B, LBO = 128 B
+// (next core matrix along K), SBO = 256 B (next 8-row group) (tools/tf32_probe.cu)
+__host__ __device__ __forceinline__ uint32_t off32(int r, int k) {
+    return (uint32_t)((r >> 3) * 256 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ uint64_t desc32(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(128u >> 4) << 16;
+    d |= (uint64_t)(256u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a), "l"(b), "r"(idesc)
+                 : "memory");
+}
+
+__device__ __forceinline__ float tf32_rna(float f) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+    return __uint_as_float(r);
+}
+
+// v = t1 + t2 + t3 (+ O(2^-33 |v|)), each part exact in tf32
+__device__ __forceinline__ void split3(double v, float &t1, float &t2, float &t3) {
+    t1 = tf32_rna((float)v);
+    const double r1 = v - (double)t1;
+    t2 = tf32_rna((float)r1);
+    t3 = tf32_rna((float)(r1 - (double)t2));
+}
+__device__ __forceinline__ void split3(float v, float &t1, float &t2, float &t3) {
+    t1 = tf32_rna(v);
+    const float r1 = v - t1;
+    t2 = tf32_rna(r1);
+    t3 = tf32_rna(r1 - t2);
+}
+
+__device__ __forceinline__ void arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// window of one tile: start sample and the bulk-copyable range [lo, hi)
+struct Win {
+    long long c, n0, start, lo, hi;
+};
+__device__ __forceinline__ Win win(long long tile, long long C, long long N, int H, int W, int vec_x) {
+    Win g;
+    g.c = (long long)((unsigned)tile % (unsigned)C);
+    g.n0 = (long long)((unsigned)tile / (unsigned)C) * (long long)CT_TOUT;
+    g.start = g.n0 - H;
+    g.lo = g.start > 0 ? g.start : 0;
+    const long long nv = vec_x ? (N & ~3LL) : 0;
+    long long hi = g.start + W;
+    if (hi > nv) hi = nv;
+    g.hi = hi > g.lo ? hi : g.lo;
+    return g;
+}
+
+// out += M v, M block lower triangular (2x2 blocks): one FMA chain per row
+// (independent rows / segments give the ILP)
+template <int D, typename TS, typename F>
+__device__ __forceinline__ void matvec_fma(TS (&out)[D], const TS (&v)[D], F m) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const int nj = 2 * ((i >> 1) + 1);
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if (j < nj) out[i] = fma(m(i, j), v[j], out[i]);
+    }
+}
+
+template <typename TS, int D>
+__device__ __forceinline__ void store_vec(TS *dst, const TS (&v)[D]) {
+    if constexpr ((sizeof(TS) * D) % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(TS) * D / 16); ++q)
+            reinterpret_cast<uint4 *>(dst)[q] = reinterpret_cast<const uint4 *>(v)[q];
+    } else {
+#pragma unroll
+        for (int d = 0; d < D; ++d) dst[d] = v[d];
+    }
+}
+
+template <typename TS, int D>
+__device__ __forceinline__ void load_vec(TS (&v)[D], const TS *src) {
+    if constexpr ((sizeof(TS) * D) % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(TS) * D / 16); ++q)
+            reinterpret_cast<uint4 *>(v)[q] = __ldcg(reinterpret_cast<const uint4 *>(src) + q);
+    } else {
+#pragma unroll
+        for (int d = 0; d < D; ++d) v[d] = ldcg(src + d);
+    }
+}
+
+}  // namespace c3d
+
+// ---------------------------------------------------------------------------
+// chain_rows: one warp per tile (persistent, static stride over tiles). Lane l
+// owns rows l, l+32, l+64, l+96: four independent 32-row SEGMENTS per tile,
+// each scanned across the warp with no CTA barrier; two segments per pass, so
+// every coefficient loaded from shared memory feeds two rows.
+template <typename TS, int S>
+__global__ void __launch_bounds__(C3_ROWS_THREADS, 4) chain_rows_kernel(const C3RowsArgs a,
+                                                                        const C3RowsTables<TS, 2 * S> tb) {
+    constexpr int D = 2 * S;
+    __shared__ __align__(16) TS Ks[64][D];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < 64 * D; i += C3_ROWS_THREADS) Ks[i / D][i % D] = tb.K[i / D][i % D];
+    __syncthreads();
+    TS *rows = reinterpret_cast<TS *>(a.rows);
+    TS *aggs = reinterpret_cast<TS *>(a.aggs);
+    const long long nwarps = (long long)gridDim.x * (C3_ROWS_THREADS / 32);
+    for (long long tile = (long long)blockIdx.x * (C3_ROWS_THREADS / 32) + (tid >> 5); tile < a.total_tiles;
+         tile += nwarps) {
+        const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
+        const long long k = (long long)((unsigned long long)tile / (unsigned long long)a.C);
+        const float *xr = a.x + c * a.ldx;
+        const long long t0 = k * CT_TOUT - a.H;
+        const bool fast = a.vec_x && t0 >= 0 && t0 + CT_TOUT <= a.N;
+        // two passes of two segments: 16 accumulators per pass, 8 samples per
+        // step per row, the next step's samples in flight
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const long long base = t0 + 64LL * lane + 4096LL * pass;  // row `lane` of segment 2 pass
+            TS e[2][D];
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int d = 0; d < D; ++d) e[g][d] = TS(0);
+            auto ld8 = [&](float4 (&v)[4], int q) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const long long pos = base + 2048 * g + 8 * q + 4 * h;
+                        v[2 * g + h] = fast ? __ldg(reinterpret_cast<const float4 *>(xr + pos))
+                                            : load_region4(xr, pos, a.N, a.vec_x);
+                    }
+            };
+            float4 cur[4];
+            ld8(cur, 0);
+#pragma unroll 1
+            for (int q = 0; q < 8; ++q) {
+                float4 nxt[4];
+                if (q < 7) ld8(nxt, q + 1);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    TS xv[2];
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        const float4 &f = cur[2 * g + (u >> 2)];
+                        const int w = u & 3;
+                        xv[g] = (TS)(w == 0 ? f.x : w == 1 ? f.y : w == 2 ? f.z : f.w);
+                    }
+                    const TS *kr = &Ks[8 * q + u][0];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) {
+                        const TS kc = kr[d];
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) e[g][d] = fma(kc, xv[g], e[g][d]);
+                    }
+                }
+                if (q < 7) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cur[j] = nxt[j];
+                }
+            }
+            // per segment: warp inclusive scan over rows, incl_t = e_t + M incl_{t-1}
+#pragma unroll
+            for (int stp = 0; stp < 5; ++stp) {
+                const int off = 1 << stp;
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    TS prev[D];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) prev[d] = shfl_up(e[g][d], off);
+                    if (lane >= off) c3d::matvec_fma<D, TS>(e[g], prev, [&](int r, int q) { return tb.P[stp][r][q]; });
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const int sg = 2 * pass + g;
+                TS Lm[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const TS u = shfl_up(e[g][d], 1);
+                    Lm[d] = lane == 0 ? TS(0) : u;
+                }
+                c3d::store_vec<TS, D>(rows + ((size_t)tile * CT_ROWS + 32 * sg + lane) * D, Lm);
+                if (lane == 31) c3d::store_vec<TS, D>(aggs + ((size_t)tile * 4 + sg) * D, e[g]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// chain_carry: one CTA per channel over its 4 T segments (segment j = tile j/4,
+// rows 32 (j%4) ..); thread t owns segments [t B, (t+1) B).
+template <typename TS, int S>
+__global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3CarryArgs a,
+                                                                       const C3CarryTables<TS, 2 * S> tb) {
+    constexpr int D = 2 * S;
+    constexpr int NWC = C3_CARRY_THREADS / 32;
+    __shared__ TS wt[NWC][D];
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const long long c = blockIdx.x;
+    const long long j0 = (long long)tid * a.B;
+    const long long j1 = j0 + a.B < a.T ? j0 + a.B : a.T;
+    const TS *aggs = reinterpret_cast<const TS *>(a.aggs);
+    TS *carry = reinterpret_cast<TS *>(a.carry);
+    auto seg = [&](long long j) { return (size_t)(((j >> 2) * a.C + c) * 4 + (j & 3)) * D; };
+    auto mt = [&](int r, int q) { return tb.MT[r][q]; };
+    // local inclusive prefix of this thread's segments (zero carry)
+    TS loc[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) loc[d] = TS(0);
+    {
+        TS nxt[D];
+        if (j0 < j1) c3d::load_vec<TS, D>(nxt, aggs + seg(j0));
+#pragma unroll 1
+        for (long long j = j0; j < j1; ++j) {
+            TS cur[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+            if (j + 1 < j1) c3d::load_vec<TS, D>(nxt, aggs + seg(j + 1));
+            c3d::matvec_fma<D, TS>(cur, loc, mt);
+#pragma unroll
+            for (int d = 0; d < D; ++d) loc[d] = cur[d];
+        }
+    }
+    // warp scan over threads (blocks of exactly B segments before any short one)
+    TS incl[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) incl[d] = loc[d];
+#pragma unroll
+    for (int stp = 0; stp < 5; ++stp) {
+        const int off = 1 << stp;
+        TS prev[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) prev[d] = shfl_up(incl[d], off);
+        if (lane >= off) ctd::matvec_tree<D, TS>(incl, prev, [&](int r, int q) { return tb.Q[stp][r][q]; });
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) wt[wq][d] = incl[d];
+    }
+    __syncthreads();
+    TS ex[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const TS u = shfl_up(incl[d], 1);
+        ex[d] = lane == 0 ? TS(0) : u;
+    }
+    {
+        // carry entering this warp (Horner): wc = MT^(32 B) wc + wt_u, u < wq
+        TS wc[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) wc[d] = TS(0);
+#pragma unroll 1
+        for (int u = 0; u < wq; ++u) {
+            TS nw[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) nw[d] = wt[u][d];
+            ctd::matvec_tree<D, TS>(nw, wc, [&](int r, int q) { return tb.R[r][q]; });
+#pragma unroll
+            for (int d = 0; d < D; ++d) wc[d] = nw[d];
+        }
+        // ex += MT^(B lane) wc: apply the Q powers by the bits of lane
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+            if ((lane >> b) & 1) {
+                TS z[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) z[d] = TS(0);
+                ctd::matvec_tree<D, TS>(z, wc, [&](int r, int q) { return tb.Q[b][r][q]; });
+#pragma unroll
+                for (int d = 0; d < D; ++d) wc[d] = z[d];
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) ex[d] += wc[d];
+    }
+    // replay: carry of each owned segment
+    {
+        TS nxt[D];
+        if (j0 < j1) c3d::load_vec<TS, D>(nxt, aggs + seg(j0));
+#pragma unroll 1
+        for (long long j = j0; j < j1; ++j) {
+            TS cur[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+            if (j + 1 < j1) c3d::load_vec<TS, D>(nxt, aggs + seg(j + 1));
+            c3d::store_vec<TS, D>(carry + seg(j), ex);
+            c3d::matvec_fma<D, TS>(cur, ex, mt);
+#pragma unroll
+            for (int d = 0; d < D; ++d) ex[d] = cur[d];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// chain_gemm: persistent, one CTA per SM, warp-specialized.
+struct C3Layout {
+    uint32_t opBytes, bBytes;
+    uint32_t rawBytes;
+    uint32_t bimg, eimg, op, sop, raw, g, stg, misc, bars;
+    uint32_t total;
+    __host__ __device__ C3Layout(int W, int K, int D, int ts) {
+        opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
+        bBytes = (uint32_t)((K + 63) / 64) * 8192u;  // one part; the image is [atom][hi rows | lo rows]
+        bimg = 0;
+        eimg = bimg + 2 * bBytes;
+        op = eimg + 3 * 2048u;
+        sop = op + 4 * opBytes;             // [2 stages][hi, lo]
+        raw = sop + 2u * 3u * 4096u;        // sop: [2 stages][3 parts][128 rows x 32 B]
+        rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
+        g = raw + rawBytes;                 // raw: one fp32 window (bulk copy)
+        stg = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
+        misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32
+        bars = (misc + 64u + 15u) & ~15u;
+        total = bars + 24 * 8 + 16 + 1024;  // + alignment slack
+    }
+};
+
+template <typename TS, int S>
+__global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a) {
+    constexpr int D = 2 * S;
+    static_assert(D <= 8, "state operand holds K = 8 columns");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nk = a.K / 16;
+    const C3Layout lay(a.W, a.K, D, (int)sizeof(TS));
+#define C3TR(tile, ev) \
+    do {                                                                              \
+        if (a.trace) a.trace[(long long)(tile) * C3_TRACE_EV + (ev)] = ctd::gtimer(); \
+    } while (0)
+    unsigned char *bimg = smem + lay.bimg;
+    unsigned char *op = smem + lay.op;
+    unsigned char *sop = smem + lay.sop;
+    TS *gsm = reinterpret_cast<TS *>(smem + lay.g);
+    unsigned char *stg = smem + lay.stg;
+    float *scl = reinterpret_cast<float *>(smem + lay.misc);  // [8] ring by local tile
+    float *red = scl + 8;                                     // [8]
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+    const uint32_t bar0 = wptc::smem_u32(bars);
+    // barriers: OP_FULL, OP_EMPTY, SOP_FULL, SOP_EMPTY x 2 stages; ACC_FULL, ACC_EMPTY x 4 stages
+#define OPF(s) (bar0 + 8u * (uint32_t)(0 + (s)))
+#define OPE(s) (bar0 + 8u * (uint32_t)(2 + (s)))
+#define SOF(s) (bar0 + 8u * (uint32_t)(4 + (s)))
+#define SOE(s) (bar0 + 8u * (uint32_t)(6 + (s)))
+#define ACF(s) (bar0 + 8u * (uint32_t)(8 + (s)))
+#define ACE(s) (bar0 + 8u * (uint32_t)(12 + (s)))
+#define RWF (bar0 + 8u * 16u)
+#define RWE (bar0 + 8u * 17u)
+
+    if (warp == 0) wptc::tmem_alloc(wptc::smem_u32(tmem_slot), 128 * C3_NA);
+    if (tid == 32) {
+        for (int s = 0; s < 2; ++s) {
+            wptc::mbar_init(OPF(s), 1);
+            wptc::mbar_init(OPE(s), 1);
+            wptc::mbar_init(SOF(s), CT_ROWS);
+            wptc::mbar_init(SOE(s), 1);
+        }
+        for (int s = 0; s < C3_NA; ++s) {
+            wptc::mbar_init(ACF(s), 1);
+            wptc::mbar_init(ACE(s), CT_ROWS);
+        }
+        wptc::mbar_init(RWF, 1);
+        wptc::mbar_init(RWE, 1);
+        wptc::mbar_fence_init();
+    }
+    for (int i = tid; i < (int)(2 * lay.bBytes / 16); i += C3_THREADS)
+        reinterpret_cast<uint4 *>(bimg)[i] = reinterpret_cast<const uint4 *>(a.Bimg)[i];
+    for (int i = tid; i < 3 * 2048 / 16; i += C3_THREADS)
+        reinterpret_cast<uint4 *>(smem + lay.eimg)[i] = reinterpret_cast<const uint4 *>(a.Eimg)[i];
+    for (int i = tid; i < 2 * 3 * 4096 / 16; i += C3_THREADS)  // state columns >= D stay zero
+        reinterpret_cast<uint4 *>(sop)[i] = make_uint4(0u, 0u, 0u, 0u);
+    {
+        const TS *G = reinterpret_cast<const TS *>(a.G);
+        for (int i = tid; i < D * D * 32; i += C3_THREADS) {
+            const int r = i / (D * 32), q = (i / 32) % D, l = i % 32;
+            if (q < lt_nj(r)) gsm[(lt_off(r) + q) * 32 + l] = G[(r * D + q) * 33 + l];
+        }
+    }
+    wptc::fence_proxy_async_smem();
+    wptc::fence_before_sync();
+    __syncthreads();
+    wptc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const long long first = blockIdx.x, stride = gridDim.x;
+    const int ntiles = first < a.total_tiles ? (int)((a.total_tiles - 1 - first) / stride + 1) : 0;
+
+    if (warp == 0) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            const uint32_t idesc = wptc::idesc_f16(128, 64), idesc2 = wptc::idesc_f16(128, 128);
+            const uint32_t idt = c3d::idesc_tf32(128, 64);
+            const uint32_t op0 = wptc::smem_u32(op), b0 = wptc::smem_u32(bimg);
+            const uint32_t sop0 = wptc::smem_u32(sop), e0 = wptc::smem_u32(smem + lay.eimg);
+            for (int i = 0; i < ntiles; ++i) {
+                const int s = i & 1;
+                const uint32_t par = (uint32_t)((i >> 1) & 1);
+                const int sa = i % C3_NA;
+                const uint32_t para = (uint32_t)((i / C3_NA) & 1);
+                wptc::mbar_wait(OPF(s), par);
+                wptc::mbar_wait(ACE(sa), para ^ 1u);
+                wptc::fence_after_sync();
+                C3TR(first + (long long)i * stride, 2);
+                // columns [0, 64): x_hi g_hi + x_lo g_hi (+ state term); [64, 128): x_hi g_lo
+                const uint32_t dm = tmem + 128u * sa;
+                const uint32_t ahi = op0 + (2u * s) * lay.opBytes, alo = ahi + lay.opBytes;
+                const uint64_t ah0 = ctd::desc_sw128(ahi), al0 = ctd::desc_sw128(alo);
+#pragma unroll 1
+                for (int kk = 0; kk < nk; ++kk) {
+                    const uint64_t ka = 2u * kk;  // +32 B per K step, across rows (Hankel)
+                    const uint64_t bb = ctd::desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
+                    wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
+                    wptc::mma_f16(dm, al0 + ka, bb, idesc, 1u);
+                }
+                C3TR(first + (long long)i * stride, 3);
+                wptc::mbar_wait(SOF(s), par);
+                wptc::fence_after_sync();
+                if (!(a.dbg & 4)) {
+                    // state term: parts (i, j) with i + j < 3 of s' x E
+#pragma unroll
+                    for (int pr = 0; pr < 6; ++pr) {
+                        // (s' part, E part): (0,0) (0,1) (1,0) (0,2) (1,1) (2,0)
+                        const int ia = pr == 2 || pr == 4 ? 1 : pr == 5 ? 2 : 0;
+                        const int ib = pr == 1 || pr == 4 ? 1 : pr == 3 ? 2 : 0;
+                        c3d::mma_tf32(dm, c3d::desc32(sop0 + (uint32_t)(s * 3 + ia) * 4096u),
+                                      c3d::desc32(e0 + (uint32_t)ib * 2048u), idt);
+                    }
+                }
+                // OPE only after SOF: the state role reads the tile's scale after
+                // waiting on OPF(s), so the converters must not complete the next
+                // OPF(s) phase before that wait (parity aliasing)
+                wptc::mma_commit(OPE(s));
+                wptc::mma_commit(SOE(s));
+                wptc::mma_commit(ACF(sa));
+            }
+        }
+    } else if (warp == 1) {
+        // ================= bulk-copy producer: fp32 window -> smem =================
+        if (lane == 0) {
+            const uint32_t raw0 = wptc::smem_u32(smem + lay.raw);
+            for (int i = 0; i < ntiles; ++i) {
+                wptc::mbar_wait(RWE, (uint32_t)(i & 1) ^ 1u);
+                const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
+                const uint32_t bytes = (uint32_t)(4 * (g.hi - g.lo));
+                if (bytes > 0) {
+                    c3d::arrive_tx(RWF, bytes);
+                    const float *src = a.x + g.c * a.ldx + g.lo;
+                    const uint32_t dst = raw0 + 4u * (uint32_t)(g.lo - g.start);
+                    // pieces of <= 16 KB
+                    for (uint32_t o = 0; o < bytes; o += 16384u) {
+                        const uint32_t nb = bytes - o < 16384u ? bytes - o : 16384u;
+                        c3d::bulk_g2s(dst + o, reinterpret_cast<const unsigned char *>(src) + o, nb, RWF);
+                    }
+                } else {
+                    ctd::arrive(RWF);
+                }
+                // warm L2 with the window after next
+                const long long nt = first + (long long)(i + 2) * stride;
+                if (i + 2 < ntiles) {
+                    const c3d::Win g2 = c3d::win(nt, a.C, a.N, a.H, a.W, a.vec_x);
+                    const uint32_t b2 = (uint32_t)(4 * (g2.hi - g2.lo));
+                    if (b2 > 0) ctd::prefetch_l2(a.x + g2.c * a.ldx + g2.lo, b2);
+                }
+            }
+        }
+    } else if (warp >= 2 && warp <= 6) {
+        // ================= converters (warps 2..6): fp32 window -> SW128 fp16 hi / lo =================
+        const int ct = tid - 64;
+        const int cw = ct >> 5;
+        const int nq = a.W / 4;
+        const float4 *raw4 = reinterpret_cast<const float4 *>(smem + lay.raw);
+        for (int i = 0; i < ntiles; ++i) {
+            const int s = i & 1;
+            const uint32_t par = (uint32_t)((i >> 1) & 1);
+            const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
+            const float *xr = a.x + g.c * a.ldx;
+            const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
+            wptc::mbar_wait(RWF, (uint32_t)(i & 1));
+            if (ct == 0) C3TR(first + (long long)i * stride, 0);
+            float4 v[CT_QMAX];
+            float m = 0.f;
+            if (interior) {
+#pragma unroll
+                for (int j = 0; j < CT_QMAX; ++j)
+                    v[j] = (ct + j * CT_CONV < nq) ? raw4[ct + j * CT_CONV] : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+#pragma unroll 1
+                for (int j = 0; j < CT_QMAX; ++j) {
+                    const int q = ct + j * CT_CONV;
+                    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (q < nq) {
+                        const long long p0 = g.start + 4LL * q;
+                        if (p0 >= g.lo && p0 + 4 <= g.hi) {
+                            t = raw4[q];
+                        } else {
+                            t.x = (p0 + 0 >= 0 && p0 + 0 < a.N) ? __ldg(xr + p0 + 0) : 0.f;
+                            t.y = (p0 + 1 >= 0 && p0 + 1 < a.N) ? __ldg(xr + p0 + 1) : 0.f;
+                            t.z = (p0 + 2 >= 0 && p0 + 2 < a.N) ? __ldg(xr + p0 + 2) : 0.f;
+                            t.w = (p0 + 3 >= 0 && p0 + 3 < a.N) ? __ldg(xr + p0 + 3) : 0.f;
+                        }
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < CT_QMAX; ++jj)
+                        if (jj == j) v[jj] = t;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CT_QMAX; ++j)
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+            const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+            if (lane == 0) red[cw] = __uint_as_float(mb);
+            ctd::named_sync(1, CT_CONV);
+            if (ct == 0) ctd::arrive(RWE);  // the window is in registers: free it
+            float tmax = red[0];
+#pragma unroll
+            for (int w = 1; w < CT_CONV / 32; ++w) tmax = fmaxf(tmax, red[w]);
+            int ex = 0;
+            if (tmax > 0.f) frexpf(tmax, &ex);
+            const float sc = ldexpf(1.f, tmax > 0.f ? 14 - ex : 0);
+            wptc::mbar_wait(OPE(s), par ^ 1u);
+            unsigned char *ohi = op + (2 * s) * lay.opBytes, *olo = ohi + lay.opBytes;
+#pragma unroll
+            for (int j = 0; j < CT_QMAX; ++j) {
+                const int q = ct + j * CT_CONV;
+                if (q < nq) {
+                    const float2 f01 = make_float2(v[j].x * sc, v[j].y * sc);
+                    const float2 f23 = make_float2(v[j].z * sc, v[j].w * sc);
+                    const __half2 h01 = __float22half2_rn(f01), h23 = __float22half2_rn(f23);
+                    const float2 b01 = __half22float2(h01), b23 = __half22float2(h23);
+                    const __half2 l01 = __floats2half2_rn(f01.x - b01.x, f01.y - b01.y);
+                    const __half2 l23 = __floats2half2_rn(f23.x - b23.x, f23.y - b23.y);
+                    uint2 hv, lv;
+                    hv.x = *reinterpret_cast<const uint32_t *>(&h01);
+                    hv.y = *reinterpret_cast<const uint32_t *>(&h23);
+                    lv.x = *reinterpret_cast<const uint32_t *>(&l01);
+                    lv.y = *reinterpret_cast<const uint32_t *>(&l23);
+                    const uint32_t off = ctd::swz128(8u * (uint32_t)q);
+                    *reinterpret_cast<uint2 *>(ohi + off) = hv;
+                    *reinterpret_cast<uint2 *>(olo + off) = lv;
+                }
+            }
+            if (ct == 0) scl[i & 7] = sc;
+            wptc::fence_proxy_async_smem();
+            ctd::named_sync(2, CT_CONV);
+            if (ct == 0) {
+                ctd::arrive(OPF(s));
+                C3TR(first + (long long)i * stride, 1);
+            }
+        }
+    } else if (warp >= 8 && warp <= 11) {
+        // ================= state operand (warps 8..11), one tile row per thread =================
+        const int wq = warp & 3;
+        const int row = 32 * wq + lane;
+        const TS *rows = reinterpret_cast<const TS *>(a.rows);
+        const TS *carry = reinterpret_cast<const TS *>(a.carry);
+        TS Ln[D], Cn[D];
+        if (ntiles > 0) {
+            c3d::load_vec<TS, D>(Ln, rows + ((size_t)first * CT_ROWS + row) * D);
+            c3d::load_vec<TS, D>(Cn, carry + ((size_t)first * 4 + wq) * D);
+        }
+        for (int i = 0; i < ntiles; ++i) {
+            const int s = i & 1;
+            const uint32_t par = (uint32_t)((i >> 1) & 1);
+            TS sv[D], cv[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) sv[d] = Ln[d], cv[d] = Cn[d];
+            if (i + 1 < ntiles) {
+                const long long nt = first + (long long)(i + 1) * stride;
+                c3d::load_vec<TS, D>(Ln, rows + ((size_t)nt * CT_ROWS + row) * D);
+                c3d::load_vec<TS, D>(Cn, carry + ((size_t)nt * 4 + wq) * D);
+            }
+            // s_m = L_m + M^lane carry(segment wq)
+            ctd::matvec_tree<D, TS>(sv, cv, [&](int r, int q) { return gsm[(lt_off(r) + q) * 32 + lane]; });
+            if (row == 0) C3TR(first + (long long)i * stride, 4);
+            wptc::mbar_wait(OPF(s), par);  // the tile's input scale
+            const TS f = (TS)scl[i & 7] * (TS)a.st_scale;
+            wptc::mbar_wait(SOE(s), par ^ 1u);
+            unsigned char *dst = sop + (size_t)s * 3 * 4096;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                float t1, t2, t3;
+                c3d::split3(sv[d] * f, t1, t2, t3);
+                const uint32_t o = c3d::off32(row, d);
+                *reinterpret_cast<float *>(dst + o) = t1;
+                *reinterpret_cast<float *>(dst + 4096 + o) = t2;
+                *reinterpret_cast<float *>(dst + 8192 + o) = t3;
+            }
+            wptc::fence_proxy_async_smem();
+            ctd::arrive(SOF(s));
+            if (row == 0) C3TR(first + (long long)i * stride, 5);
+        }
+    } else if (warp >= 12) {
+        // ================= epilogue (warps 12..15): TMEM -> scale -> coalesced stores =================
+        const int wq = warp & 3;
+        const uint32_t trow = (uint32_t)(32 * wq) << 16;
+        unsigned char *mystg = stg + (size_t)wq * 32 * CT_STG_PITCH;
+        for (int i = 0; i < ntiles; ++i) {
+            const int sa = i % C3_NA;
+            const long long tile = first + (long long)i * stride;
+            const long long c = (long long)((unsigned)tile % (unsigned)a.C);
+            const long long n0 = (long long)((unsigned)tile / (unsigned)a.C) * (long long)CT_TOUT;
+            wptc::mbar_wait(ACF(sa), (uint32_t)((i / C3_NA) & 1));
+            wptc::fence_after_sync();
+            if (tid == 384) C3TR(tile, 6);
+            const float osc = a.out_scale / scl[i & 7];
+            const uint32_t tbase = tmem + 128u * sa + trow;
+            float *yr = a.y + c * a.ldy + n0;
+            const long long tleft = a.N - n0;
+            const bool full = a.vec_y && tleft >= CT_TOUT;
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+                const int h = ch >> 1, hh = ch & 1;
+                float t16[16], u16[16];
+                ctd::tmem_ld16(tbase + 16u * ch, t16);
+                ctd::tmem_ld16(tbase + 64u + 16u * ch, u16);
+                wptc::tmem_wait_ld();
+                if (ch == 3) {
+                    wptc::fence_before_sync();
+                    ctd::arrive(ACE(sa));
+                }
+                float4 *dst = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                    dst[q4] = make_float4((t16[4 * q4] + u16[4 * q4]) * osc, (t16[4 * q4 + 1] + u16[4 * q4 + 1]) * osc,
+                                          (t16[4 * q4 + 2] + u16[4 * q4 + 2]) * osc,
+                                          (t16[4 * q4 + 3] + u16[4 * q4 + 3]) * osc);
+                if (hh == 1) {
+                    __syncwarp();
+                    if (full) {
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            const int q = lane + 32 * r;
+                            const int rr = q >> 3, c4 = q & 7;
+                            const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * CT_STG_PITCH + 16 * c4);
+                            __stcs(reinterpret_cast<float4 *>(yr + 64 * (32 * wq + rr) + 32 * h + 4 * c4), v);
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int r = 0; r < 8; ++r) {
+                            const int q = lane + 32 * r;
+                            const int rr = q >> 3, c4 = q & 7;
+                            const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * CT_STG_PITCH + 16 * c4);
+                            const int o = 64 * (32 * wq + rr) + 32 * h + 4 * c4;
+                            const long long left = tleft - o;
+                            if (a.vec_y && left >= 4) {
+                                __stcs(reinterpret_cast<float4 *>(yr + o), v);
+                            } else {
+                                if (left > 0) yr[o + 0] = v.x;
+                                if (left > 1) yr[o + 1] = v.y;
+                                if (left > 2) yr[o + 2] = v.z;
+                                if (left > 3) yr[o + 3] = v.w;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            if (tid == 384) C3TR(tile, 7);
+        }
+    }
+#undef C3TR
+#undef OPF
+#undef OPE
+#undef SOF
+#undef SOE
+#undef ACF
+#undef ACE
+#undef RWF
+#undef RWE
+    wptc::fence_before_sync();
+    __syncthreads();
+    wptc::fence_after_sync();
+    if (warp == 0) wptc::tmem_dealloc(tmem, 128 * C3_NA);
+}
+
+}  // namespace wpk

@@ -506,6 +506,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1)
                 int spins = 0;
                 while ((f >> 2) != a.epoch || (f & 3ull) < (unsigned long long)need || f < want) {
                     if (++spins > 8) __nanosleep(spins < 64 ? 20 : 100);
+                    if ((spins & 0x3FFFFFF) == 0) __trap();  // watchdog: ~64M polls without progress
                     f = ld_acquire(&src->flag);
                 }
                 const TS *sv = need == 2 ? src->incl : src->agg;

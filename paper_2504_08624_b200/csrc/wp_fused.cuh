@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(NT, 3) fused_chain_kernel(const FusedArgs a, c
                     int spins = 0;
                     while ((f >> 2) != a.epoch || (f & 3ull) < (unsigned long long)need || f < want) {
                         if (++spins > 4) __nanosleep(spins < 64 ? 32 : 256);
+                        if ((spins & 0x3FFFFFF) == 0) __trap();  // watchdog: ~64M polls (> 15 s) without progress
                         f = ld_acquire(&src->flag);
                     }
                     const TS *sv = need == 2 ? src->incl : src->agg;

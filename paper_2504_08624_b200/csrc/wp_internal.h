@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "wp_chain3.cuh"
 #include "wp_chain_tc.cuh"
 #include "wp_fused.cuh"
 
@@ -88,6 +89,18 @@ int fir_tc_occupancy(size_t smem);
 size_t chain_tc_smem_bytes(int W, int K, int S, bool f64);
 cudaError_t launch_chain_tc(bool f64, int S, const wpk::ChainTcArgs &a, const HostTables &t,
                             const std::vector<double> &E, int grid, size_t smem, cudaStream_t st);
+
+// decoupled tensor-core chain (wp_chain3.cu): chain_rows -> chain_carry -> chain_gemm
+struct Chain3Launch {
+    wpk::C3RowsArgs rows;
+    wpk::C3CarryArgs carry;
+    wpk::C3GemmArgs gemm;
+    std::vector<double> carry_mats;  // [7][D][D]: MT = M^32, MT^(B 2^i) i < 5, MT^(32 B)
+    int gemm_grid = 1;
+    size_t smem = 0;
+};
+size_t chain3_smem_bytes(int W, int K, int S, bool f64);
+cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st);
 
 // WAV payload codec (wp_wav.cu)
 cudaError_t launch_wav_decode(const void *payload, int enc, float *y, long long C, long long N, long long ld,

@@ -78,15 +78,31 @@ __device__ __forceinline__ void mbar_fence_init() {
 // Blocking wait on an mbarrier phase. The suspend-time hint lets the waiting
 // warp sleep in hardware until the phase completes instead of re-polling the
 // barrier (spinning warps otherwise eat issue slots and shared-memory pipe
-// bandwidth that the producer warps need).
-__device__ __forceinline__ void mbar_wait(uint32_t saddr, uint32_t parity) {
+// bandwidth that the producer warps need). Watchdog: a wait that has not
+// completed after 10 s traps, so a pipeline bug aborts the launch with an
+// error instead of hanging the device.
+__device__ __forceinline__ bool mbar_try(uint32_t saddr, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
-        "@!done bra WAIT_%=;\n\t}\n" ::"r"(saddr),
-        "r"(parity), "r"(1000000u)
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, done;\n\t}\n"
+        : "=r"(ok)
+        : "r"(saddr), "r"(parity), "r"(1000000u)
         : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t saddr, uint32_t parity) {
+    if (mbar_try(saddr, parity)) return;
+    const unsigned long long t0 = now_ns();
+    while (!mbar_try(saddr, parity)) {
+        if (now_ns() - t0 > 10000000000ull) asm volatile("trap;");
+    }
 }
 
 // 32 lanes x 32 bit, 8 consecutive columns per thread
