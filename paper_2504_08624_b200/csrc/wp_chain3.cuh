@@ -428,8 +428,8 @@ struct C3Layout {
         rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         g = raw + rawBytes;                 // raw: one fp32 window (bulk copy)
         stg = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
-        misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32
-        bars = (misc + 64u + 15u) & ~15u;
+        misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32, stag[8] i32
+        bars = (misc + 96u + 15u) & ~15u;
         total = bars + 24 * 8 + 16 + 1024;  // + alignment slack
     }
 };
@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
     unsigned char *stg = smem + lay.stg;
     float *scl = reinterpret_cast<float *>(smem + lay.misc);  // [8] ring by local tile
     float *red = scl + 8;                                     // [8]
+    int *stag = reinterpret_cast<int *>(red + 8);             // [8] local tile index of scl[]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
     const uint32_t bar0 = wptc::smem_u32(bars);
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
         reinterpret_cast<uint4 *>(smem + lay.eimg)[i] = reinterpret_cast<const uint4 *>(a.Eimg)[i];
     for (int i = tid; i < 2 * 3 * 4096 / 16; i += C3_THREADS)  // state columns >= D stay zero
         reinterpret_cast<uint4 *>(sop)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid < 8) stag[tid] = -1;
     {
         const TS *G = reinterpret_cast<const TS *>(a.G);
         for (int i = tid; i < D * D * 32; i += C3_THREADS) {
@@ -531,6 +533,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                     wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
                     wptc::mma_f16(dm, al0 + ka, bb, idesc, 1u);
                 }
+                wptc::mma_commit(OPE(s));  // the operand stage is free once the main GEMM has read it
                 C3TR(first + (long long)i * stride, 3);
                 wptc::mbar_wait(SOF(s), par);
                 wptc::fence_after_sync();
@@ -548,7 +551,6 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                 // OPE only after SOF: the state role reads the tile's scale after
                 // waiting on OPF(s), so the converters must not complete the next
                 // OPF(s) phase before that wait (parity aliasing)
-                wptc::mma_commit(OPE(s));
                 wptc::mma_commit(SOE(s));
                 wptc::mma_commit(ACF(sa));
             }
@@ -658,7 +660,11 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                     *reinterpret_cast<uint2 *>(olo + off) = lv;
                 }
             }
-            if (ct == 0) scl[i & 7] = sc;
+            if (ct == 0) {
+                scl[i & 7] = sc;
+                __threadfence_block();
+                *reinterpret_cast<volatile int *>(stag + (i & 7)) = i;
+            }
             wptc::fence_proxy_async_smem();
             ctd::named_sync(2, CT_CONV);
             if (ct == 0) {
@@ -691,7 +697,13 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
             // s_m = L_m + M^lane carry(segment wq)
             ctd::matvec_tree<D, TS>(sv, cv, [&](int r, int q) { return gsm[(lt_off(r) + q) * 32 + lane]; });
             if (row == 0) C3TR(first + (long long)i * stride, 4);
-            wptc::mbar_wait(OPF(s), par);  // the tile's input scale
+            // the tile's input scale: tagged ring slot (absolute local tile index,
+            // so no barrier-phase aliasing however far the converters run ahead)
+            for (int spins = 0; *reinterpret_cast<volatile int *>(stag + (i & 7)) != i; ++spins) {
+                __nanosleep(32);
+                if (spins > (1 << 28)) __trap();  // watchdog
+            }
+            __threadfence_block();
             const TS f = (TS)scl[i & 7] * (TS)a.st_scale;
             wptc::mbar_wait(SOE(s), par ^ 1u);
             unsigned char *dst = sop + (size_t)s * 3 * 4096;
