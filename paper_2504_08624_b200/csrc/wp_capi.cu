@@ -698,7 +698,7 @@ void free_pass(Pass &p) {
 size_t rec_bytes(const Pass &p) {
     if (p.kind != Pass::FUSED || p.S == 0) return 0;
     const size_t es = p.f64 ? 8 : 4;
-    if (p.chain3) return (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 8);  // row prefixes, segment aggregates + carries
+    if (p.chain3) return (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 5);  // row prefixes, tile aggregate, 4 carries
     return (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
 }
 
@@ -953,16 +953,15 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             const size_t es = p.f64 ? 8 : 4;
             unsigned char *rows = ws + rec_off;
             unsigned char *aggs = rows + (size_t)tiles * wpk::CT_ROWS * D * es;
-            unsigned char *carry = aggs + (size_t)tiles * 4 * D * es;
+            unsigned char *carry = aggs + (size_t)tiles * D * es;
             const int vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
             const int vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
             L.rows = wpk::C3RowsArgs{in, C, N, ld_in, tiles, p.ct_H, vec_x, p.d_G, rows, aggs};
-            const long long segs = 4 * T;
-            const int B = (int)((segs + wpk::C3_CARRY_THREADS - 1) / wpk::C3_CARRY_THREADS);
-            L.carry = wpk::C3CarryArgs{C, segs, B, aggs, carry};
+            const int B = (int)((T + wpk::C3_CARRY_THREADS - 1) / wpk::C3_CARRY_THREADS);
+            L.carry = wpk::C3CarryArgs{C, T, B, aggs, carry};
             {
-                // segment transfer M^32 = W[1]; thread-block and warp powers
-                const Mat MT(p.tables.W.begin() + (size_t)D * D, p.tables.W.begin() + (size_t)2 * D * D);
+                // tile transfer M^128; thread-block and warp powers
+                const Mat &MT = p.tables.MT;
                 const Mat MB = matpow(MT, B, D);
                 L.carry_mats.assign((size_t)7 * D * D, 0.0);
                 std::copy(MT.begin(), MT.end(), L.carry_mats.begin());

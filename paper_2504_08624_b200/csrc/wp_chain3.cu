@@ -15,9 +15,22 @@ wpk::C3RowsTables<TS, 2 * S> c3_rows_tables(const HostTables &t) {
     wpk::C3RowsTables<TS, D> tb{};
     for (int n = 0; n < 64; ++n)
         for (int i = 0; i < D; ++i) tb.K[n][i] = TS(t.K[n * D + i]);
-    for (int q = 0; q < 5; ++q)
+    // P[q] = M^(2^q), q < 7 (the host tables hold q < 5)
+    std::vector<double> m(t.P.begin() + 4 * D * D, t.P.begin() + 5 * D * D);
+    for (int q = 0; q < 7; ++q) {
+        if (q >= 5) {
+            std::vector<double> m2((size_t)D * D, 0.0);
+            for (int i = 0; i < D; ++i)
+                for (int j = 0; j < D; ++j) {
+                    long double acc = 0;
+                    for (int l = 0; l < D; ++l) acc += (long double)m[i * D + l] * m[l * D + j];
+                    m2[i * D + j] = (double)acc;
+                }
+            m = m2;
+        }
         for (int i = 0; i < D; ++i)
-            for (int j = 0; j < D; ++j) tb.P[q][i][j] = TS(t.P[(q * D + i) * D + j]);
+            for (int j = 0; j < D; ++j) tb.P[q][i][j] = TS(q < 5 ? t.P[(q * D + i) * D + j] : m[i * D + j]);
+    }
     for (int w = 0; w < 4; ++w)
         for (int i = 0; i < D; ++i)
             for (int j = 0; j < D; ++j) tb.W[w][i][j] = TS(t.W[(w * D + i) * D + j]);
@@ -31,14 +44,17 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     // chain_rows: persistent, as many CTAs as fit
     static int rows_occ = 0;
     if (!rows_occ) {
+        cudaError_t e = cudaFuncSetAttribute(wpk::chain_rows_kernel<TS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             wpk::C3_ROWS_SMEM);
+        if (e != cudaSuccess) return e;
         int occ = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>,
-                                                                      wpk::C3_ROWS_THREADS, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>, wpk::C3_ROWS_THREADS,
+                                                          wpk::C3_ROWS_SMEM);
         if (e != cudaSuccess) return e;
         rows_occ = std::max(occ, 1);
     }
     const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ * sm_count());
-    wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, 0, st>>>(L.rows, tb);
+    wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, wpk::C3_ROWS_SMEM, st>>>(L.rows, tb);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -49,6 +65,7 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
             ct.MT[i][j] = TS(L.carry_mats[i * D + j]);
             for (int q = 0; q < 5; ++q) ct.Q[q][i][j] = TS(L.carry_mats[((1 + q) * D + i) * D + j]);
             ct.R[i][j] = TS(L.carry_mats[(6 * D + i) * D + j]);
+            for (int w = 0; w < 3; ++w) ct.W[w][i][j] = TS(t.W[((w + 1) * D + i) * D + j]);
         }
     wpk::chain_carry_kernel<TS, S><<<(unsigned)L.carry.C, wpk::C3_CARRY_THREADS, 0, st>>>(L.carry, ct);
     count_launch();
@@ -58,7 +75,11 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     auto kern = wpk::chain_gemm_kernel<TS, S>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
-    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm);
+    wpk::C3WTables<TS, D> wt{};
+    for (int w = 0; w < 4; ++w)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) wt.W[w][i][j] = TS(t.W[(w * D + i) * D + j]);
+    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm, wt);
     count_launch();
     return cudaGetLastError();
 }

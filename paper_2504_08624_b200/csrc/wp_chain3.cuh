@@ -50,29 +50,30 @@ struct C3RowsArgs {
     int H;
     int vec_x;
     const void *G;  // [D][D][33] TS, M^l lane-minor
-    void *rows;     // [tiles][128][D] TS: zero-carry prefixes within each 32-row segment
-    void *aggs;     // [tiles][4][D] TS: segment aggregates
+    void *rows;     // [tiles][128][D] TS: zero-carry row prefixes within the tile
+    void *aggs;     // [tiles][D] TS: tile aggregates
 };
 
 template <typename TS, int D>
 struct C3RowsTables {
     TS K[64][D];     // A^(63-j) B
-    TS P[5][D][D];   // M^(2^i)
+    TS P[7][D][D];   // M^(2^i)
     TS W[4][D][D];   // M^(32 w)
 };
 
 struct C3CarryArgs {
-    long long C, T;  // channels, segments per channel (4 per tile)
-    int B;           // segments per thread
+    long long C, T;  // channels, tiles per channel
+    int B;           // tiles per thread
     const void *aggs;
-    void *carry;     // [tiles][4][D] TS: state entering each segment
+    void *carry;     // [tiles][4][D] TS: state entering rows 0, 32, 64, 96 of each tile
 };
 
 template <typename TS, int D>
 struct C3CarryTables {
-    TS MT[D][D];     // M^32: one segment
+    TS MT[D][D];     // M^128: one tile
     TS Q[5][D][D];   // MT^(B 2^i)
     TS R[D][D];      // MT^(32 B): one warp of threads
+    TS W[3][D][D];   // M^(32 w), w = 1..3: carries of a tile's row quarters
 };
 
 struct C3GemmArgs {
@@ -207,107 +208,157 @@ __device__ __forceinline__ void load_vec(TS (&v)[D], const TS *src) {
 }  // namespace c3d
 
 // ---------------------------------------------------------------------------
-// chain_rows: one warp per tile (persistent, static stride over tiles). Lane l
-// owns rows l, l+32, l+64, l+96: four independent 32-row SEGMENTS per tile,
-// each scanned across the warp with no CTA barrier; two segments per pass, so
-// every coefficient loaded from shared memory feeds two rows.
+// chain_rows: one warp per tile (persistent, static stride over tiles), no CTA
+// barrier. Lane l owns rows 4l..4l+3: four independent e accumulations (every
+// coefficient read from shared memory feeds four rows), a serial scan over its
+// four rows, one Kogge-Stone over the lanes, and the rows' exclusive prefixes.
+// The samples stream through a per-warp ring of C3_RSTG shared-memory stages
+// (8 samples x 128 rows each) filled by cp.async, C3_RSTG - 1 steps ahead.
+constexpr int C3_RSTG = 4;
+constexpr int C3_ROWS_SMEM = (C3_ROWS_THREADS / 32) * C3_RSTG * 4096;  // dynamic: the sample rings
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// byte offset of (row, 16-byte half h) inside a stage: rows of 32 B, four rows
+// per 128-B line; the 16-B chunk position is XOR-swizzled by the line index so
+// that lanes reading rows 4l + g (g fixed) hit distinct banks
+__device__ __forceinline__ uint32_t rs_off(int row, int h) {
+    return (uint32_t)((row >> 2) * 128 + 16 * ((((row & 3) << 1) | h) ^ ((row >> 2) & 7)));
+}
+
 template <typename TS, int S>
-__global__ void __launch_bounds__(C3_ROWS_THREADS, 4) chain_rows_kernel(const C3RowsArgs a,
+__global__ void __launch_bounds__(C3_ROWS_THREADS, 3) chain_rows_kernel(const C3RowsArgs a,
                                                                         const C3RowsTables<TS, 2 * S> tb) {
     constexpr int D = 2 * S;
+    constexpr int NWR = C3_ROWS_THREADS / 32;
     __shared__ __align__(16) TS Ks[64][D];
-    const int tid = threadIdx.x, lane = tid & 31;
+    extern __shared__ __align__(16) unsigned char ring[];  // [NWR][C3_RSTG][128 rows x 32 B]
+    const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
     for (int i = tid; i < 64 * D; i += C3_ROWS_THREADS) Ks[i / D][i % D] = tb.K[i / D][i % D];
     __syncthreads();
     TS *rows = reinterpret_cast<TS *>(a.rows);
     TS *aggs = reinterpret_cast<TS *>(a.aggs);
-    const long long nwarps = (long long)gridDim.x * (C3_ROWS_THREADS / 32);
-    for (long long tile = (long long)blockIdx.x * (C3_ROWS_THREADS / 32) + (tid >> 5); tile < a.total_tiles;
-         tile += nwarps) {
+    unsigned char *myring = ring + (size_t)wr * C3_RSTG * 4096;
+    const uint32_t ring0 = wptc::smem_u32(myring);
+    // this lane's copy chunks: rows (lane >> 1) + 16 j, half lane & 1
+    uint32_t soff[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) soff[j] = rs_off((lane >> 1) + 16 * j, lane & 1);
+    const long long nwarps = (long long)gridDim.x * NWR;
+    auto mt1 = [&](int r, int q) { return tb.P[0][r][q]; };  // M: one row
+    for (long long tile = (long long)blockIdx.x * NWR + wr; tile < a.total_tiles; tile += nwarps) {
         const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
         const long long k = (long long)((unsigned long long)tile / (unsigned long long)a.C);
         const float *xr = a.x + c * a.ldx;
         const long long t0 = k * CT_TOUT - a.H;
         const bool fast = a.vec_x && t0 >= 0 && t0 + CT_TOUT <= a.N;
-        // two passes of two segments: 16 accumulators per pass, 8 samples per
-        // step per row, the next step's samples in flight
+        const float *gp = xr + t0 + 64 * (lane >> 1) + 4 * (lane & 1);
+        auto fill = [&](int q) {
+            const uint32_t so = (uint32_t)(q % C3_RSTG) * 4096u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (fast) {
+                    cp_async16(ring0 + so + soff[j], gp + 1024 * j + 8 * q);
+                } else {
+                    const long long pos = t0 + 64LL * ((lane >> 1) + 16 * j) + 8 * q + 4 * (lane & 1);
+                    *reinterpret_cast<float4 *>(myring + so + soff[j]) = load_region4(xr, pos, a.N, a.vec_x);
+                }
+            }
+        };
+        __syncwarp();  // the previous tile's reads of the ring are done
+#pragma unroll
+        for (int q = 0; q < C3_RSTG - 1; ++q) {
+            fill(q);
+            cp_async_commit();
+        }
+        // lane l: rows 4 l + g
+        TS e[4][D];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int d = 0; d < D; ++d) e[g][d] = TS(0);
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-            const long long base = t0 + 64LL * lane + 4096LL * pass;  // row `lane` of segment 2 pass
-            TS e[2][D];
+        for (int q = 0; q < 8; ++q) {
+            if (q + C3_RSTG - 1 < 8) fill(q + C3_RSTG - 1);
+            cp_async_commit();
+            cp_async_wait<C3_RSTG - 1>();
+            __syncwarp();
+            const unsigned char *stg = myring + (q % C3_RSTG) * 4096;
 #pragma unroll
-            for (int g = 0; g < 2; ++g)
+            for (int h = 0; h < 2; ++h) {
+                float4 xv4[4];
 #pragma unroll
-                for (int d = 0; d < D; ++d) e[g][d] = TS(0);
-            auto ld8 = [&](float4 (&v)[4], int q) {
+                for (int g = 0; g < 4; ++g) xv4[g] = *reinterpret_cast<const float4 *>(stg + rs_off(4 * lane + g, h));
 #pragma unroll
-                for (int g = 0; g < 2; ++g)
+                for (int u = 0; u < 4; ++u) {
+                    TS xv[4];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const long long pos = base + 2048 * g + 8 * q + 4 * h;
-                        v[2 * g + h] = fast ? __ldg(reinterpret_cast<const float4 *>(xr + pos))
-                                            : load_region4(xr, pos, a.N, a.vec_x);
-                    }
-            };
-            float4 cur[4];
-            ld8(cur, 0);
-#pragma unroll 1
-            for (int q = 0; q < 8; ++q) {
-                float4 nxt[4];
-                if (q < 7) ld8(nxt, q + 1);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    TS xv[2];
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-                        const float4 &f = cur[2 * g + (u >> 2)];
-                        const int w = u & 3;
-                        xv[g] = (TS)(w == 0 ? f.x : w == 1 ? f.y : w == 2 ? f.z : f.w);
-                    }
-                    const TS *kr = &Ks[8 * q + u][0];
+                    for (int g = 0; g < 4; ++g)
+                        xv[g] = (TS)(u == 0 ? xv4[g].x : u == 1 ? xv4[g].y : u == 2 ? xv4[g].z : xv4[g].w);
+                    const TS *kr = &Ks[8 * q + 4 * h + u][0];
 #pragma unroll
                     for (int d = 0; d < D; ++d) {
                         const TS kc = kr[d];
 #pragma unroll
-                        for (int g = 0; g < 2; ++g) e[g][d] = fma(kc, xv[g], e[g][d]);
+                        for (int g = 0; g < 4; ++g) e[g][d] = fma(kc, xv[g], e[g][d]);
                     }
                 }
-                if (q < 7) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) cur[j] = nxt[j];
-                }
             }
-            // per segment: warp inclusive scan over rows, incl_t = e_t + M incl_{t-1}
+            __syncwarp();  // stage q is refilled C3_RSTG - 1 steps later
+        }
+        // serial scan over the lane's 4 rows (zero carry), then a Kogge-Stone over
+        // lanes with M^(4 2^i), then the rows' exclusive prefixes
+        TS t[D];
 #pragma unroll
-            for (int stp = 0; stp < 5; ++stp) {
-                const int off = 1 << stp;
+        for (int d = 0; d < D; ++d) t[d] = e[0][d];
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    TS prev[D];
+        for (int g = 1; g < 4; ++g) {
+            TS nt[D];
 #pragma unroll
-                    for (int d = 0; d < D; ++d) prev[d] = shfl_up(e[g][d], off);
-                    if (lane >= off) c3d::matvec_fma<D, TS>(e[g], prev, [&](int r, int q) { return tb.P[stp][r][q]; });
-                }
-            }
+            for (int d = 0; d < D; ++d) nt[d] = e[g][d];
+            c3d::matvec_fma<D, TS>(nt, t, mt1);
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                const int sg = 2 * pass + g;
-                TS Lm[D];
+            for (int d = 0; d < D; ++d) t[d] = nt[d];
+        }
 #pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    const TS u = shfl_up(e[g][d], 1);
-                    Lm[d] = lane == 0 ? TS(0) : u;
-                }
-                c3d::store_vec<TS, D>(rows + ((size_t)tile * CT_ROWS + 32 * sg + lane) * D, Lm);
-                if (lane == 31) c3d::store_vec<TS, D>(aggs + ((size_t)tile * 4 + sg) * D, e[g]);
+        for (int stp = 0; stp < 5; ++stp) {
+            const int off = 1 << stp;
+            TS prev[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) prev[d] = shfl_up(t[d], off);
+            if (lane >= off) c3d::matvec_fma<D, TS>(t, prev, [&](int r, int q) { return tb.P[stp + 2][r][q]; });
+        }
+        if (lane == 31) c3d::store_vec<TS, D>(aggs + (size_t)tile * D, t);
+        TS Lm[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const TS u = shfl_up(t[d], 1);
+            Lm[d] = lane == 0 ? TS(0) : u;
+        }
+        TS *dst = rows + ((size_t)tile * CT_ROWS + 4 * lane) * D;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            c3d::store_vec<TS, D>(dst + g * D, Lm);
+            if (g < 3) {
+                TS nl[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) nl[d] = e[g][d];
+                c3d::matvec_fma<D, TS>(nl, Lm, mt1);
+#pragma unroll
+                for (int d = 0; d < D; ++d) Lm[d] = nl[d];
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// chain_carry: one CTA per channel over its 4 T segments (segment j = tile j/4,
-// rows 32 (j%4) ..); thread t owns segments [t B, (t+1) B).
+// chain_carry: one CTA per channel over its T tiles; thread t owns tiles
+// [t B, (t+1) B).
 template <typename TS, int S>
 __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3CarryArgs a,
                                                                        const C3CarryTables<TS, 2 * S> tb) {
@@ -320,7 +371,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
     const long long j1 = j0 + a.B < a.T ? j0 + a.B : a.T;
     const TS *aggs = reinterpret_cast<const TS *>(a.aggs);
     TS *carry = reinterpret_cast<TS *>(a.carry);
-    auto seg = [&](long long j) { return (size_t)(((j >> 2) * a.C + c) * 4 + (j & 3)) * D; };
+    auto seg = [&](long long j) { return (size_t)(j * a.C + c) * D; };
     auto mt = [&](int r, int q) { return tb.MT[r][q]; };
     // local inclusive prefix of this thread's segments (zero carry)
     TS loc[D];
@@ -402,7 +453,17 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
 #pragma unroll
             for (int d = 0; d < D; ++d) cur[d] = nxt[d];
             if (j + 1 < j1) c3d::load_vec<TS, D>(nxt, aggs + seg(j + 1));
-            c3d::store_vec<TS, D>(carry + seg(j), ex);
+            // state entering rows 0, 32, 64, 96 of tile j
+            TS *cq = carry + seg(j) * 4;
+            c3d::store_vec<TS, D>(cq, ex);
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                TS vq[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) vq[d] = TS(0);
+                c3d::matvec_fma<D, TS>(vq, ex, [&](int r, int q) { return tb.W[w][r][q]; });
+                c3d::store_vec<TS, D>(cq + (w + 1) * D, vq);
+            }
             c3d::matvec_fma<D, TS>(cur, ex, mt);
 #pragma unroll
             for (int d = 0; d < D; ++d) ex[d] = cur[d];
@@ -415,7 +476,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
 struct C3Layout {
     uint32_t opBytes, bBytes;
     uint32_t rawBytes;
-    uint32_t bimg, eimg, op, sop, raw, g, stg, misc, bars;
+    uint32_t bimg, eimg, op, sop, raw, g, ws, stg, misc, bars;
     uint32_t total;
     __host__ __device__ C3Layout(int W, int K, int D, int ts) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
@@ -427,15 +488,21 @@ struct C3Layout {
         raw = sop + 2u * 3u * 4096u;        // sop: [2 stages][3 parts][128 rows x 32 B]
         rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         g = raw + rawBytes;                 // raw: one fp32 window (bulk copy)
-        stg = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
+        ws = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
+        stg = (ws + (uint32_t)(ts * 4 * D * D) + 15u) & ~15u;
         misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32, stag[8] i32
         bars = (misc + 96u + 15u) & ~15u;
         total = bars + 24 * 8 + 16 + 1024;  // + alignment slack
     }
 };
 
+template <typename TS, int D>
+struct C3WTables {
+    TS W[4][D][D];  // M^(32 w)
+};
+
 template <typename TS, int S>
-__global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a) {
+__global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a, const C3WTables<TS, 2 * S> wt) {
     constexpr int D = 2 * S;
     static_assert(D <= 8, "state operand holds K = 8 columns");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -451,6 +518,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
     unsigned char *op = smem + lay.op;
     unsigned char *sop = smem + lay.sop;
     TS *gsm = reinterpret_cast<TS *>(smem + lay.g);
+    TS *Ws = reinterpret_cast<TS *>(smem + lay.ws);  // [4][D][D]
     unsigned char *stg = smem + lay.stg;
     float *scl = reinterpret_cast<float *>(smem + lay.misc);  // [8] ring by local tile
     float *red = scl + 8;                                     // [8]
@@ -497,6 +565,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
             const int r = i / (D * 32), q = (i / 32) % D, l = i % 32;
             if (q < lt_nj(r)) gsm[(lt_off(r) + q) * 32 + l] = G[(r * D + q) * 33 + l];
         }
+        for (int i = tid; i < 4 * D * D; i += C3_THREADS) Ws[i] = wt.W[i / (D * D)][(i / D) % D][i % D];
     }
     wptc::fence_proxy_async_smem();
     wptc::fence_before_sync();
@@ -694,7 +763,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                 c3d::load_vec<TS, D>(Ln, rows + ((size_t)nt * CT_ROWS + row) * D);
                 c3d::load_vec<TS, D>(Cn, carry + ((size_t)nt * 4 + wq) * D);
             }
-            // s_m = L_m + M^lane carry(segment wq)
+            // s_m = L_m + M^lane (M^(32 wq) carry)
             ctd::matvec_tree<D, TS>(sv, cv, [&](int r, int q) { return gsm[(lt_off(r) + q) * 32 + lane]; });
             if (row == 0) C3TR(first + (long long)i * stride, 4);
             // the tile's input scale: tagged ring slot (absolute local tile index,
