@@ -75,11 +75,7 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     auto kern = wpk::chain_gemm_kernel<TS, S>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
-    wpk::C3WTables<TS, D> wt{};
-    for (int w = 0; w < 4; ++w)
-        for (int i = 0; i < D; ++i)
-            for (int j = 0; j < D; ++j) wt.W[w][i][j] = TS(t.W[(w * D + i) * D + j]);
-    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm, wt);
+    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm);
     count_launch();
     return cudaGetLastError();
 }

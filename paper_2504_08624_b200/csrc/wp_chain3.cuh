@@ -90,7 +90,7 @@ struct C3GemmArgs {
     const void *rows;           // [tiles][128][D] TS
     const void *carry;          // [tiles][4][D] TS
     int vec_x, vec_y;
-    int dbg;                    // 4 = no state term
+    int dbg;                    // diagnostics: 4 = no state term
     unsigned long long *trace;  // optional: [tiles][C3_TRACE_EV] globaltimer stamps
 };
 constexpr int C3_TRACE_EV = 8;
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
 struct C3Layout {
     uint32_t opBytes, bBytes;
     uint32_t rawBytes;
-    uint32_t bimg, eimg, op, sop, raw, g, ws, stg, misc, bars;
+    uint32_t bimg, eimg, op, sop, raw, g, stg, misc, bars;
     uint32_t total;
     __host__ __device__ C3Layout(int W, int K, int D, int ts) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
@@ -488,21 +488,15 @@ struct C3Layout {
         raw = sop + 2u * 3u * 4096u;        // sop: [2 stages][3 parts][128 rows x 32 B]
         rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         g = raw + rawBytes;                 // raw: one fp32 window (bulk copy)
-        ws = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
-        stg = (ws + (uint32_t)(ts * 4 * D * D) + 15u) & ~15u;
+        stg = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
         misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32, stag[8] i32
         bars = (misc + 96u + 15u) & ~15u;
         total = bars + 24 * 8 + 16 + 1024;  // + alignment slack
     }
 };
 
-template <typename TS, int D>
-struct C3WTables {
-    TS W[4][D][D];  // M^(32 w)
-};
-
 template <typename TS, int S>
-__global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a, const C3WTables<TS, 2 * S> wt) {
+__global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a) {
     constexpr int D = 2 * S;
     static_assert(D <= 8, "state operand holds K = 8 columns");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -518,7 +512,6 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
     unsigned char *op = smem + lay.op;
     unsigned char *sop = smem + lay.sop;
     TS *gsm = reinterpret_cast<TS *>(smem + lay.g);
-    TS *Ws = reinterpret_cast<TS *>(smem + lay.ws);  // [4][D][D]
     unsigned char *stg = smem + lay.stg;
     float *scl = reinterpret_cast<float *>(smem + lay.misc);  // [8] ring by local tile
     float *red = scl + 8;                                     // [8]
@@ -565,7 +558,6 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
             const int r = i / (D * 32), q = (i / 32) % D, l = i % 32;
             if (q < lt_nj(r)) gsm[(lt_off(r) + q) * 32 + l] = G[(r * D + q) * 33 + l];
         }
-        for (int i = tid; i < 4 * D * D; i += C3_THREADS) Ws[i] = wt.W[i / (D * D)][(i / D) % D][i % D];
     }
     wptc::fence_proxy_async_smem();
     wptc::fence_before_sync();

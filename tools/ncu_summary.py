@@ -58,6 +58,7 @@ def main():
     kernels = raw(report)
     md = [f"# {title}", "", f"report: `{os.path.basename(report)}` (ncu --set full --clock-control none)", ""]
     summary = {}
+    tot_bytes, tot_us, names = 0.0, 0.0, []
     for name, m in kernels:
         md.append(f"## `{name[:110]}`")
         md.append("")
@@ -69,11 +70,20 @@ def main():
         wr = to_bytes(*m["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in m else None
         if rd is not None and wr is not None:
             md.append(f"| dram bytes per launch (read+write) | {rd + wr:.4e} |")
-            summary = {"kernel": name[:120], "dram_bytes_per_launch": rd + wr,
-                       "duration_us": (float(m["gpu__time_duration.sum"][0]) * {"ms": 1e3, "us": 1.0, "ns": 1e-3}.get(
-                           m["gpu__time_duration.sum"][1], 1.0)) if "gpu__time_duration.sum" in m else None,
-                       "report": os.path.basename(report)}
+            us = (float(m["gpu__time_duration.sum"][0]) * {"ms": 1e3, "us": 1.0, "ns": 1e-3}.get(
+                m["gpu__time_duration.sum"][1], 1.0)) if "gpu__time_duration.sum" in m else 0.0
+            tot_bytes += rd + wr
+            tot_us += us
+            names.append(name.split("(")[0][:60])
         md.append("")
+    if names:
+        # one pass may be several kernels (chain_rows + chain_carry + chain_gemm):
+        # traffic and time are summed over the kernels of the report
+        summary = {"kernel": " + ".join(names), "dram_bytes_per_launch": tot_bytes, "duration_us": tot_us,
+                   "kernels_in_pass": len(names), "report": os.path.basename(report)}
+        if len(names) > 1:
+            md.append(f"**pass total** ({len(names)} kernels): DRAM {tot_bytes:.4e} B, {tot_us:.1f} us (serialised, cold)")
+            md.append("")
     if launches and os.path.exists(launches):
         md.append("## launch list (`--metrics gpu__time_duration.sum`, cold cache, serialised)")
         md.append("")
