@@ -424,3 +424,71 @@ def test_many_channels_lp8_subset_parity():
     for c in (0, 1, 150, 299):
         ref = oracle.pipe(w.samples[c:c + 1], [lp8.bind(fs)])
         assert oracle.parity_error(y[c:c + 1], ref) <= IIR_TOL, c
+
+
+# ---- the three-kernel chain (chain_rows -> chain_carry -> chain_gemm) ---------
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [2, 4, 6, 8])
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+@pytest.mark.parametrize("taps", [2, 16, 101, 129])
+def test_chain_pass_matrix_vs_oracle(order, precision, taps):
+    """Every section count x scan dtype x FIR length the tensor-core chain
+    accepts, on ragged frame counts around the 8192-sample tile."""
+    fs = 48000
+    kind = "hp" if order % 4 == 0 else "lp"
+    # f32 scans only for moderate pole radii (the planner picks f64 above 0.98)
+    fc = (150 if precision == "f64" else 1500) if kind == "hp" else 3000
+    stages = [wp.design_butterworth(kind, order, fc, fs),
+              wp.design_fir("lp", taps, 12000, fs=fs) if taps > 2 else wp.FirFilter.from_taps([0.75, 0.25], fs),
+              wp.Gain(0.5)]
+    rng = np.random.default_rng(order * 1000 + taps)
+    wp.set_iir_precision(precision)
+    try:
+        for frames in (8191, 8193, 40001):
+            w = wp.Wave(rng.standard_normal((3, frames)), fs)
+            y = wp.pipe(w, wp.Chain(stages)).samples
+            ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
+            assert oracle.parity_error(y, ref) <= IIR_TOL, (frames, precision)
+    finally:
+        wp.set_iir_precision("auto")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [1, 4, 8])
+def test_chain_pass_iir_only_forced(order, monkeypatch):
+    """IIR-only passes through the three-kernel chain (H = 0, K = 64) when it
+    is forced; the default planner keeps them on the fused kernel."""
+    import torch
+
+    fs = 48000
+    filt = wp.design_butterworth("lp", order, 2000, fs)
+    bound = wp.Chain([filt]).bind(fs).stages
+    monkeypatch.setenv("WP_CHAIN_IMPL", "tc")
+    plan = _native.Plan(tuple(wp.engine._entry(s) for s in bound))  # uncached: the env var applies
+    assert "chain_gemm" in plan.describe()[0]
+    rng = np.random.default_rng(order)
+    C, N = 5, 60001
+    x = rng.standard_normal((C, N)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    nb = plan.workspace_bytes(C, N)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    plan.execute(xd.data_ptr(), yd.data_ptr(), C, N, N, N, ws.data_ptr(), nb, torch.cuda.current_stream().cuda_stream)
+    ref = oracle.iir_cascade(filt.sos_rows(), x.astype(np.float64))
+    assert oracle.parity_error(yd.cpu().numpy().astype(np.float64), ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+def test_chain_pass_stopband_input_f64():
+    """The hard case for the state term: a low-frequency sine through cfg3's
+    100 Hz high-pass, where the output is the small difference of the window
+    and state terms."""
+    fs = 48000
+    n = np.arange(3 * 8192 + 77)
+    x = np.stack([0.9 * np.sin(2 * np.pi * 30 * n / fs), 0.5 * np.sin(2 * np.pi * 12 * n / fs + 1.0)])
+    stages = _cfg3()
+    y = wp.pipe(wp.Wave(x, fs), wp.Chain(stages)).samples
+    ref = oracle.pipe(np.asarray(x, np.float32).astype(np.float64), wp.Chain(stages).bind(fs).stages)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
