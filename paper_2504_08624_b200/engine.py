@@ -270,9 +270,9 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     """Host -> device -> host execution of a recorded chain, overlapped.
 
     ``host_src`` and ``host_out`` are pinned float32 CPU tensors ``[C, N]``.
-    Channels are cut into pair-aligned blocks (channels are independent, and
-    the FFT path filters pairs together, so results are bit-identical to one
-    launch over all channels); block b's upload, the fused pass over block
+    Channels are cut into blocks (single channels, or pairs when a pass runs
+    the FFT path, which filters pairs together; results are bit-identical to
+    one launch over all channels); block b's upload, the fused pass over block
     b-1 and block b-2's download run concurrently on three streams, so the
     PCIe link carries both directions at once instead of one after the other.
     """
@@ -284,13 +284,17 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     _require_cuda()
     C, N = host_src.shape
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    nblk = blocks or max(1, min((C + 1) // 2, 32))
-    parts = [(a, b) for a, b in partition(C, nblk) if b > a]
     with torch.cuda.device(dev):
+        plan = _plans.get(dev.index, entries)
+        # the FFT path filters channel pairs together: keep its blocks pair-aligned;
+        # every other pass is per channel, so single-channel blocks shorten the
+        # first-upload / last-download ramp
+        pairs = any(d.startswith("fft_ols") for d in plan.describe())
+        nblk = blocks or (max(1, min((C + 1) // 2, 32)) if pairs else max(1, min(C, 64)))
+        parts = [(a, b) for a, b in partition(C, nblk, align=2 if pairs else 1) if b > a]
         s_in, s_run, s_out = _copy_streams(dev)
         x = torch.empty((C, N), dtype=torch.float32, device=dev)
         y = torch.empty_like(x)
-        plan = _plans.get(dev.index, entries)
         ws = _workspace(dev, s_run.cuda_stream, max(plan.workspace_bytes(b - a, N) for a, b in parts))
         cur = torch.cuda.current_stream(dev)
         s_in.wait_stream(cur)
