@@ -45,16 +45,16 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     static int rows_occ = 0;
     if (!rows_occ) {
         cudaError_t e = cudaFuncSetAttribute(wpk::chain_rows_kernel<TS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             wpk::C3_ROWS_SMEM);
+                                             wpk::c3_rows_smem<TS>());
         if (e != cudaSuccess) return e;
         int occ = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>, wpk::C3_ROWS_THREADS,
-                                                          wpk::C3_ROWS_SMEM);
+                                                          wpk::c3_rows_smem<TS>());
         if (e != cudaSuccess) return e;
         rows_occ = std::max(occ, 1);
     }
     const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ * sm_count());
-    wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, wpk::C3_ROWS_SMEM, st>>>(L.rows, tb);
+    wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, wpk::c3_rows_smem<TS>(), st>>>(L.rows, tb);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -212,10 +212,16 @@ __device__ __forceinline__ void load_vec(TS (&v)[D], const TS *src) {
 // barrier. Lane l owns rows 4l..4l+3: four independent e accumulations (every
 // coefficient read from shared memory feeds four rows), a serial scan over its
 // four rows, one Kogge-Stone over the lanes, and the rows' exclusive prefixes.
-// The samples stream through a per-warp ring of C3_RSTG shared-memory stages
-// (8 samples x 128 rows each) filled by cp.async, C3_RSTG - 1 steps ahead.
-constexpr int C3_RSTG = 4;
-constexpr int C3_ROWS_SMEM = (C3_ROWS_THREADS / 32) * C3_RSTG * 4096;  // dynamic: the sample rings
+// The samples stream through a per-warp ring of RSTG shared-memory stages
+// (8 samples x 128 rows each) filled by cp.async, RSTG - 1 steps ahead: four
+// stages at 3 CTAs/SM for the fp64 scan (register-bound), three stages at 4
+// CTAs/SM for fp32 (measured best for each).
+template <typename TS>
+__host__ __device__ constexpr int c3_rstg() { return sizeof(TS) == 8 ? 4 : 3; }
+template <typename TS>
+__host__ __device__ constexpr int c3_rows_ctas() { return sizeof(TS) == 8 ? 3 : 4; }
+template <typename TS>
+__host__ __device__ constexpr int c3_rows_smem() { return (C3_ROWS_THREADS / 32) * c3_rstg<TS>() * 4096; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -231,12 +237,25 @@ __device__ __forceinline__ uint32_t rs_off(int row, int h) {
     return (uint32_t)((row >> 2) * 128 + 16 * ((((row & 3) << 1) | h) ^ ((row >> 2) & 7)));
 }
 
+// edge / unaligned tiles: guarded loads straight into the stage (kept out of
+// line so the hot loop's code stays small)
+static __device__ __noinline__ void rows_fill_slow(unsigned char *stage, const float *xr, long long t0, int q, int lane,
+                                            long long N, int vec_x) {
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+        const int row = (lane >> 1) + 16 * j;
+        const long long pos = t0 + 64LL * row + 8 * q + 4 * (lane & 1);
+        *reinterpret_cast<float4 *>(stage + rs_off(row, lane & 1)) = load_region4(xr, pos, N, vec_x);
+    }
+}
+
 template <typename TS, int S>
-__global__ void __launch_bounds__(C3_ROWS_THREADS, 3) chain_rows_kernel(const C3RowsArgs a,
+__global__ void __launch_bounds__(C3_ROWS_THREADS, c3_rows_ctas<TS>()) chain_rows_kernel(const C3RowsArgs a,
                                                                         const C3RowsTables<TS, 2 * S> tb) {
     constexpr int D = 2 * S;
     constexpr int NWR = C3_ROWS_THREADS / 32;
     __shared__ __align__(16) TS Ks[64][D];
+    constexpr int C3_RSTG = c3_rstg<TS>();
     extern __shared__ __align__(16) unsigned char ring[];  // [NWR][C3_RSTG][128 rows x 32 B]
     const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
     for (int i = tid; i < 64 * D; i += C3_ROWS_THREADS) Ks[i / D][i % D] = tb.K[i / D][i % D];
@@ -260,14 +279,11 @@ __global__ void __launch_bounds__(C3_ROWS_THREADS, 3) chain_rows_kernel(const C3
         const float *gp = xr + t0 + 64 * (lane >> 1) + 4 * (lane & 1);
         auto fill = [&](int q) {
             const uint32_t so = (uint32_t)(q % C3_RSTG) * 4096u;
+            if (fast) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (fast) {
-                    cp_async16(ring0 + so + soff[j], gp + 1024 * j + 8 * q);
-                } else {
-                    const long long pos = t0 + 64LL * ((lane >> 1) + 16 * j) + 8 * q + 4 * (lane & 1);
-                    *reinterpret_cast<float4 *>(myring + so + soff[j]) = load_region4(xr, pos, a.N, a.vec_x);
-                }
+                for (int j = 0; j < 8; ++j) cp_async16(ring0 + so + soff[j], gp + 1024 * j + 8 * q);
+            } else {
+                rows_fill_slow(myring + so, xr, t0, q, lane, a.N, a.vec_x);
             }
         };
         __syncwarp();  // the previous tile's reads of the ring are done
