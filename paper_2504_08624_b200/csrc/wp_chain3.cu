@@ -42,22 +42,31 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     constexpr int D = 2 * S;
     const wpk::C3RowsTables<TS, D> tb = c3_rows_tables<TS, S>(t);
     // chain_rows: persistent, as many CTAs as fit
-    static int rows_occ = 0;
-    if (!rows_occ) {
-        cudaError_t e = cudaFuncSetAttribute(wpk::chain_rows_kernel<TS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             wpk::c3_rows_smem<TS>());
-        if (e != cudaSuccess) return e;
+    static int rows_occ[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = dev < 0 || dev >= 64 ? 0 : dev;
+    cudaError_t e = cudaFuncSetAttribute(wpk::chain_rows_kernel<TS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         wpk::c3_rows_smem<TS>());
+    if (e != cudaSuccess) return e;
+    if (!rows_occ[dev]) {
         int occ = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>, wpk::C3_ROWS_THREADS,
                                                           wpk::c3_rows_smem<TS>());
         if (e != cudaSuccess) return e;
-        rows_occ = std::max(occ, 1);
+        rows_occ[dev] = std::max(occ, 1);
     }
-    const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ * sm_count());
+    const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ[dev] * sm_count());
     wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, wpk::c3_rows_smem<TS>(), st>>>(L.rows, tb);
     count_launch();
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    // chain_carry and chain_gemm use programmatic dependent launch: their CTAs
+    // may start while the previous kernel drains; they wait (griddepcontrol)
+    // before reading its output
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
     // chain_carry: one CTA per channel
     wpk::C3CarryTables<TS, D> ct{};
     for (int i = 0; i < D; ++i)
@@ -67,7 +76,16 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
             ct.R[i][j] = TS(L.carry_mats[(6 * D + i) * D + j]);
             for (int w = 0; w < 3; ++w) ct.W[w][i][j] = TS(t.W[((w + 1) * D + i) * D + j]);
         }
-    wpk::chain_carry_kernel<TS, S><<<(unsigned)L.carry.C, wpk::C3_CARRY_THREADS, 0, st>>>(L.carry, ct);
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)L.carry.C);
+        cfg.blockDim = dim3(wpk::C3_CARRY_THREADS);
+        cfg.stream = st;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, wpk::chain_carry_kernel<TS, S>, L.carry, ct);
+        if (e != cudaSuccess) return e;
+    }
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -75,7 +93,17 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     auto kern = wpk::chain_gemm_kernel<TS, S>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
-    kern<<<L.gemm_grid, wpk::C3_THREADS, L.smem, st>>>(L.gemm);
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)L.gemm_grid);
+        cfg.blockDim = dim3(wpk::C3_THREADS);
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = st;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, L.gemm);
+        if (e != cudaSuccess) return e;
+    }
     count_launch();
     return cudaGetLastError();
 }

@@ -141,6 +141,11 @@ __device__ __forceinline__ void split3(float v, float &t1, float &t2, float &t3)
     t3 = tf32_rna(r1 - t2);
 }
 
+// programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait until the previous kernel has completed and flushed
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void arrive_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(C3_ROWS_THREADS, c3_rows_ctas<TS>()) chain_row
     constexpr int C3_RSTG = c3_rstg<TS>();
     extern __shared__ __align__(16) unsigned char ring[];  // [NWR][C3_RSTG][128 rows x 32 B]
     const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+    c3d::pdl_trigger();  // chain_carry may be scheduled; it waits for this grid to finish
     for (int i = tid; i < 64 * D; i += C3_ROWS_THREADS) Ks[i / D][i % D] = tb.K[i / D][i % D];
     __syncthreads();
     TS *rows = reinterpret_cast<TS *>(a.rows);
@@ -388,6 +394,8 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
     const TS *aggs = reinterpret_cast<const TS *>(a.aggs);
     TS *carry = reinterpret_cast<TS *>(a.carry);
     auto seg = [&](long long j) { return (size_t)(j * a.C + c) * D; };
+    c3d::pdl_trigger();  // chain_gemm may start its main GEMMs
+    c3d::pdl_wait();     // chain_rows' aggregates are complete
     auto mt = [&](int r, int q) { return tb.MT[r][q]; };
     // local inclusive prefix of this thread's segments (zero carry)
     TS loc[D];
@@ -756,6 +764,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
         const TS *rows = reinterpret_cast<const TS *>(a.rows);
         const TS *carry = reinterpret_cast<const TS *>(a.carry);
         TS Ln[D], Cn[D];
+        c3d::pdl_wait();  // row prefixes and carries of chain_rows / chain_carry are complete
         if (ntiles > 0) {
             c3d::load_vec<TS, D>(Ln, rows + ((size_t)first * CT_ROWS + row) * D);
             c3d::load_vec<TS, D>(Cn, carry + ((size_t)first * 4 + wq) * D);
