@@ -570,7 +570,8 @@ int finalize_pass(Pass &p) {
         const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
         const size_t smem = chain_single_kernel() ? wp::chain_tc_smem_bytes(W, K, p.S, f64)
                                                   : wp::chain3_smem_bytes(W, K, p.S, f64);
-        if (W / 4 <= wpk::CT_QMAX * wpk::CT_CONV && smem <= 227 * 1024) {
+        const int qcap = chain_single_kernel() ? wpk::CT_QMAX * wpk::CT_CONV : wpk::C3_QMAX * wpk::C3_CONV;
+        if (W / 4 <= qcap && smem <= 227 * 1024) {
             int rc = build_chain_tc(p, H, K, W, f64, smem);
             if (rc != WP_OK) return rc;
             return WP_OK;

@@ -39,7 +39,9 @@
 namespace wpk {
 
 constexpr int C3_THREADS = 512;
-constexpr int C3_NA = 4;          // TMEM accumulator stages (64 columns each)
+constexpr int C3_NA = 4;          // TMEM accumulator stages (128 columns each)
+constexpr int C3_CONV = 192;      // converter threads (warps 2..7)
+constexpr int C3_QMAX = 11;       // float4 of the window per converter thread (W <= 8448)
 constexpr int C3_ROWS_THREADS = 128;
 constexpr int C3_CARRY_THREADS = 256;
 
@@ -669,8 +671,8 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                 }
             }
         }
-    } else if (warp >= 2 && warp <= 6) {
-        // ================= converters (warps 2..6): fp32 window -> SW128 fp16 hi / lo =================
+    } else if (warp >= 2 && warp <= 7) {
+        // ================= converters (warps 2..7): fp32 window -> SW128 fp16 hi / lo =================
         const int ct = tid - 64;
         const int cw = ct >> 5;
         const int nq = a.W / 4;
@@ -683,16 +685,16 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
             const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
             wptc::mbar_wait(RWF, (uint32_t)(i & 1));
             if (ct == 0) C3TR(first + (long long)i * stride, 0);
-            float4 v[CT_QMAX];
+            float4 v[C3_QMAX];
             float m = 0.f;
             if (interior) {
 #pragma unroll
-                for (int j = 0; j < CT_QMAX; ++j)
-                    v[j] = (ct + j * CT_CONV < nq) ? raw4[ct + j * CT_CONV] : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < C3_QMAX; ++j)
+                    v[j] = (ct + j * C3_CONV < nq) ? raw4[ct + j * C3_CONV] : make_float4(0.f, 0.f, 0.f, 0.f);
             } else {
 #pragma unroll 1
-                for (int j = 0; j < CT_QMAX; ++j) {
-                    const int q = ct + j * CT_CONV;
+                for (int j = 0; j < C3_QMAX; ++j) {
+                    const int q = ct + j * C3_CONV;
                     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (q < nq) {
                         const long long p0 = g.start + 4LL * q;
@@ -706,28 +708,28 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                         }
                     }
 #pragma unroll
-                    for (int jj = 0; jj < CT_QMAX; ++jj)
+                    for (int jj = 0; jj < C3_QMAX; ++jj)
                         if (jj == j) v[jj] = t;
                 }
             }
 #pragma unroll
-            for (int j = 0; j < CT_QMAX; ++j)
+            for (int j = 0; j < C3_QMAX; ++j)
                 m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
             const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
             if (lane == 0) red[cw] = __uint_as_float(mb);
-            ctd::named_sync(1, CT_CONV);
+            ctd::named_sync(1, C3_CONV);
             if (ct == 0) ctd::arrive(RWE);  // the window is in registers: free it
             float tmax = red[0];
 #pragma unroll
-            for (int w = 1; w < CT_CONV / 32; ++w) tmax = fmaxf(tmax, red[w]);
+            for (int w = 1; w < C3_CONV / 32; ++w) tmax = fmaxf(tmax, red[w]);
             int ex = 0;
             if (tmax > 0.f) frexpf(tmax, &ex);
             const float sc = ldexpf(1.f, tmax > 0.f ? 14 - ex : 0);
             wptc::mbar_wait(OPE(s), par ^ 1u);
             unsigned char *ohi = op + (2 * s) * lay.opBytes, *olo = ohi + lay.opBytes;
 #pragma unroll
-            for (int j = 0; j < CT_QMAX; ++j) {
-                const int q = ct + j * CT_CONV;
+            for (int j = 0; j < C3_QMAX; ++j) {
+                const int q = ct + j * C3_CONV;
                 if (q < nq) {
                     const float2 f01 = make_float2(v[j].x * sc, v[j].y * sc);
                     const float2 f23 = make_float2(v[j].z * sc, v[j].w * sc);
@@ -751,7 +753,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                 *reinterpret_cast<volatile int *>(stag + (i & 7)) = i;
             }
             wptc::fence_proxy_async_smem();
-            ctd::named_sync(2, CT_CONV);
+            ctd::named_sync(2, C3_CONV);
             if (ct == 0) {
                 ctd::arrive(OPF(s));
                 C3TR(first + (long long)i * stride, 1);
