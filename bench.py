@@ -346,7 +346,7 @@ def main():
 
     hbm_peak, bf16_peak, peak_kind = load_peaks()
     algo_bytes = 8.0 * units  # fp32 read once + write once per channel-sample
-    passes = plan.describe()
+    passes = plan.describe_for(C, N)
     kernel_names = {"chain_tc": "wpk::chain_tc_kernel", "fir_tc": "wpk::fir_tc_kernel",
                     "chain_rows+chain_carry+chain_gemm":
                         "wpk::chain_rows_kernel + wpk::chain_carry_kernel + wpk::chain_gemm_kernel",
@@ -380,7 +380,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": per_launch_ms,
-                     "kernel": " + ".join(kernels) + f" ({plan.launches} launch(es) per step)"},
+                     "kernel": " + ".join(kernels) + f" ({plan.launches_for(C, N)} launch(es) per step)"},
         "e2e": {"value": units * world / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,
                 "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned)"},

@@ -90,6 +90,10 @@ int wp_plan_num_passes(const wp_plan *plan);
 int wp_plan_launches(const wp_plan *plan);
 /* Human-readable description of pass i (kernel kind, sections, taps, precision). */
 const char *wp_plan_describe(const wp_plan *plan, int32_t pass);
+/* The same for one call shape: IIR-only passes run the fused scan kernel for
+ * small calls and the three-kernel tensor-core chain for large ones. */
+int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames);
+const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t channels, int64_t frames);
 
 /* ---- seam-level one-shot entry points (mirror _kernels_jit functions) ----
  * Each builds a transient plan, executes it, and frees it after the stream

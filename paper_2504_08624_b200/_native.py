@@ -42,6 +42,8 @@ EXPORTED = (
     "wp_plan_num_passes",
     "wp_plan_launches",
     "wp_plan_describe",
+    "wp_plan_launches_for",
+    "wp_plan_describe_for",
     "wp_iir_cascade",
     "wp_fir",
     "wp_white_noise",
@@ -94,6 +96,9 @@ def load(require_device: bool = False):
             lib.wp_plan_launches.argtypes = [vp]
             lib.wp_plan_describe.argtypes = [vp, i32]
             lib.wp_plan_describe.restype = ctypes.c_char_p
+            lib.wp_plan_launches_for.argtypes = [vp, i64, i64]
+            lib.wp_plan_describe_for.argtypes = [vp, i32, i64, i64]
+            lib.wp_plan_describe_for.restype = ctypes.c_char_p
             lib.wp_iir_cascade.argtypes = [dp, i32, vp, vp, i64, i64, i64, i64, i32, vp, sz, vp]
             lib.wp_fir.argtypes = [dp, i32, vp, vp, i64, i64, i64, i64, i32, vp, sz, vp]
             lib.wp_white_noise.argtypes = [vp, i64, i64, i64, ctypes.c_uint64, vp]
@@ -104,7 +109,7 @@ def load(require_device: bool = False):
             lib.wp_wav_decode.argtypes = [vp, i32, vp, i64, i64, i64, vp]
             lib.wp_wav_encode.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp]
             for name in ("wp_plan_create", "wp_plan_destroy", "wp_plan_workspace_bytes", "wp_plan_execute",
-                         "wp_plan_num_passes", "wp_plan_launches", "wp_iir_cascade", "wp_fir",
+                         "wp_plan_num_passes", "wp_plan_launches", "wp_plan_launches_for", "wp_iir_cascade", "wp_fir",
                          "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace",
                          "wp_wav_decode", "wp_wav_encode"):
                 getattr(lib, name).restype = ctypes.c_int
@@ -198,6 +203,15 @@ class Plan:
 
     def describe(self):
         return [self._lib.wp_plan_describe(self.handle, i).decode() for i in range(self.num_passes)]
+
+    def describe_for(self, channels: int, frames: int):
+        """Kernels each pass launches for this call shape (IIR-only passes
+        switch from the fused scan to the three-kernel chain on large calls)."""
+        return [self._lib.wp_plan_describe_for(self.handle, i, channels, frames).decode()
+                for i in range(self.num_passes)]
+
+    def launches_for(self, channels: int, frames: int) -> int:
+        return int(self._lib.wp_plan_launches_for(self.handle, channels, frames))
 
     def workspace_bytes(self, channels: int, frames: int) -> int:
         out = ctypes.c_size_t()

@@ -241,6 +241,13 @@ struct Pass {
     bool chain3 = false;
     unsigned char *d_Eimg = nullptr;  // tf32 parts of the state-term matrix E
     double c3_st_scale = 1.0;
+    // IIR-only passes keep the fused kernel for small calls and switch to the
+    // three-kernel chain from c3_min_tiles tiles on (both built at plan time)
+    bool c3_large = false;
+    long long c3_min_tiles = 0;
+    size_t c3_smem = 0;
+    int c3_grid_cap = 0;
+    std::string c3_desc;
     std::string desc;
     bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
 };
@@ -541,6 +548,16 @@ int build_fft(Pass &p) {
     return WP_OK;
 }
 
+void free_pass_c3(Pass &q) {
+    if (q.d_Bimg) cudaFree(q.d_Bimg);
+    if (q.d_Eimg) cudaFree(q.d_Eimg);
+    if (q.d_G) cudaFree(q.d_G);
+    if (q.d_TP) cudaFree(q.d_TP);
+    if (q.d_Bk) cudaFree(q.d_Bk);
+    q.d_Bimg = q.d_Eimg = q.d_Bk = nullptr;
+    q.d_G = q.d_TP = nullptr;
+}
+
 int finalize_pass(Pass &p) {
     if (p.kind != Pass::FUSED) {
         char buf[128];
@@ -559,6 +576,41 @@ int finalize_pass(Pass &p) {
     // on the CUDA-core chunked scan, which measured faster for them (cfg5
     // slice 295 vs 254 G ch-s/s, cfg3's IIR part 0.97 vs 1.25 ms;
     // tools/iir_probe.py). WP_CHAIN_IMPL=tc forces the tensor-core kernel.
+    if (p.S > 0 && p.T == 0 && chain_tc_enabled() && !chain_tc_forced()) {
+        // large IIR-only calls: the three-kernel chain beats the fused scan
+        // (cfg5: 42.5 vs 47.7 ms); small ones keep the fused kernel (fewer
+        // launches; exact per-chunk recurrence for the known-answer cases)
+        double rmax = 0;
+        for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
+        const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
+        const int W = wpk::CT_TOUT, K = 64;
+        const size_t smem = wp::chain3_smem_bytes(W, K, p.S, f64);
+        if (smem <= 227 * 1024) {
+            Pass q = p;
+            int rc = build_chain_tc(q, 0, K, W, f64, smem);
+            if (rc != WP_OK) {
+                free_pass_c3(q);
+                return rc;
+            }
+            p.d_Bimg = q.d_Bimg;
+            p.d_Eimg = q.d_Eimg;
+            p.ct_H = q.ct_H;
+            p.ct_K = q.ct_K;
+            p.ct_W = q.ct_W;
+            p.ct_out_scale = q.ct_out_scale;
+            p.c3_st_scale = q.c3_st_scale;
+            p.ct_E = q.ct_E;
+            p.c3_smem = q.smem;
+            p.c3_grid_cap = q.grid_cap;
+            p.c3_desc = q.desc;
+            p.c3_large = true;
+            p.c3_min_tiles = 8LL * wp::sm_count();
+            // the fused build below uploads the same scan tables (H = 0)
+            if (q.d_G) cudaFree(q.d_G);
+            if (q.d_TP) cudaFree(q.d_TP);
+            if (q.d_Bk) cudaFree(q.d_Bk);
+        }
+    }
     if (p.S > 0 && chain_tc_enabled() && (p.T > 1 || chain_tc_forced())) {
         const int T = p.T > 0 ? p.T : 1;
         const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
@@ -676,6 +728,7 @@ int finalize_pass(Pass &p) {
     snprintf(buf, sizeof buf, "fused[pre=%g iir=%d%s fir=%d post=%zu] tile=%d halo=%d smem=%zu occ=%d", (double)p.pre, p.S,
              p.S ? (p.f64 ? "(f64)" : "(f32)") : "", p.T, p.post.size(), p.Lout, p.H, p.smem, occ);
     p.desc = buf;
+    if (p.c3_large) p.desc += " ; from " + std::to_string(p.c3_min_tiles) + " tiles: " + p.c3_desc;
     return WP_OK;
 }
 
@@ -699,8 +752,10 @@ void free_pass(Pass &p) {
 size_t rec_bytes(const Pass &p) {
     if (p.kind != Pass::FUSED || p.S == 0) return 0;
     const size_t es = p.f64 ? 8 : 4;
-    if (p.chain3) return (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 5);  // row prefixes, tile aggregate, 4 carries
-    return (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
+    const size_t c3b = (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 5);  // row prefixes, tile aggregate, 4 carries
+    if (p.chain3) return c3b;
+    const size_t fb = (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
+    return p.c3_large ? std::max(fb, c3b) : fb;
 }
 
 long long tiles_per_channel(const Pass &p, long long N) { return (N + p.Lout - 1) / p.Lout; }
@@ -864,6 +919,24 @@ int wp_plan_launches(const wp_plan *plan) {
     return n;
 }
 
+static bool uses_c3(const Pass &p, int64_t C, int64_t N) {
+    return p.chain3 || (p.c3_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.c3_min_tiles);
+}
+
+int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames) {
+    if (!plan) return 0;
+    int n = 0;
+    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : uses_c3(p, channels, frames) ? 3 : 1;
+    return n;
+}
+
+const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t channels, int64_t frames) {
+    if (!plan || pass < 0 || pass >= (int)plan->passes.size()) return "";
+    const Pass &p = plan->passes[pass];
+    if (p.c3_large) return uses_c3(p, channels, frames) ? p.c3_desc.c_str() : p.desc.c_str();
+    return p.desc.c_str();
+}
+
 const char *wp_plan_describe(const wp_plan *plan, int32_t pass) {
     if (!plan || pass < 0 || pass >= (int)plan->passes.size()) return "";
     return plan->passes[pass].desc.c_str();
@@ -945,7 +1018,7 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             const int grid = (int)std::min<long long>(a.total, p.grid_cap);
             e = wp::launch_fft_ols(a, grid, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
-        } else if (p.chain3) {
+        } else if (p.chain3 || (p.c3_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.c3_min_tiles)) {
             wp::Chain3Launch L;
             const long long T = (N + wpk::CT_TOUT - 1) / wpk::CT_TOUT;
             const long long tiles = T * C;
@@ -1000,8 +1073,8 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
                 g.dbg = dv ? std::atoi(dv) : 0;
             }
             g.trace = (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV) ? g_trace : nullptr;
-            L.gemm_grid = (int)std::min<long long>(tiles, p.grid_cap);
-            L.smem = p.smem;
+            L.gemm_grid = (int)std::min<long long>(tiles, p.chain3 ? p.grid_cap : p.c3_grid_cap);
+            L.smem = p.chain3 ? p.smem : p.c3_smem;
             e = wp::launch_chain3(p.f64, p.S, L, p.tables, stream);
             if (e != cudaSuccess) return cuda_fail(e, "chain3 launch");
         } else if (p.chain_tc) {

@@ -321,22 +321,24 @@ def test_fir_tensor_core_zeros_and_tail():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize(
-    "stages, fs, kernel",
+    "stages, fs, shape, kernel",
     [
         (lambda: [wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
-                  wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, "chain_gemm"),   # cfg3
-        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, "fused"),                 # cfg5
-        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, "fused"),                 # cfg1
-        (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, "fir_tc"),            # cfg2
-        (lambda: [wp.design_fir("lp", 4096, 2000, "hamming")], 48000, "fft_ols"),          # cfg4
+                  wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, (32, 5760000), "chain_gemm"),  # cfg3
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1024, 14400000), "chain_gemm"),      # cfg5
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (4, 48000), "fused"),                 # small IIR
+        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, (2, 441000), "fused"),                # cfg1
+        (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, (8, 2880000), "fir_tc"),          # cfg2
+        (lambda: [wp.design_fir("lp", 4096, 2000, "hamming")], 48000, (128, 28800000), "fft_ols"),     # cfg4
     ],
 )
-def test_plan_uses_intended_kernel(stages, fs, kernel):
+def test_plan_uses_intended_kernel(stages, fs, shape, kernel):
     from paper_2504_08624_b200 import engine
 
     plan = engine.plan_for(wp.Chain(stages()).bind(fs).stages, device=0)
-    desc = plan.describe()
+    desc = plan.describe_for(*shape)
     assert len(desc) == 1 and kernel in desc[0].split("[")[0], desc
+    assert plan.launches_for(*shape) == (3 if kernel == "chain_gemm" else 1)
 
 
 # ---- host -> device -> host streaming (pinned sources, channel blocks) -------
