@@ -357,7 +357,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(name, {}).get("dram_bytes_per_launch")
+            ent = json.load(open(prof)).get(name, {})
+            # a profile taken on a slice of this config scales per channel-sample
+            traffic = ent["dram_bytes_per_unit"] * units if "dram_bytes_per_unit" in ent else ent.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     clocks = clk.summary()

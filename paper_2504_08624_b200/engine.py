@@ -286,11 +286,11 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):
         plan = _plans.get(dev.index, entries)
-        # the FFT path filters channel pairs together: keep its blocks pair-aligned;
-        # every other pass is per channel, so single-channel blocks shorten the
-        # first-upload / last-download ramp
+        # the FFT path filters channel pairs together: keep its blocks pair-aligned
+        # (every other pass is per channel); ~16-32 blocks balance the
+        # first-upload / last-download ramp against per-block launch overhead
         pairs = any(d.startswith("fft_ols") for d in plan.describe())
-        nblk = blocks or (max(1, min((C + 1) // 2, 32)) if pairs else max(1, min(C, 64)))
+        nblk = blocks or max(1, min((C + 1) // 2, 32))
         parts = [(a, b) for a, b in partition(C, nblk, align=2 if pairs else 1) if b > a]
         s_in, s_run, s_out = _copy_streams(dev)
         x = torch.empty((C, N), dtype=torch.float32, device=dev)

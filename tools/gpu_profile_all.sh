@@ -1,11 +1,17 @@
-# Round profiling pass: launch lists + ncu --set full captures of the hot kernels.
-# Reports land in gpurun_out/; summarise here with tools/ncu_summary.py.
+# Round profiling pass: per-kernel launch lists + ncu --set full captures of the
+# chain kernels (cfg3, cfg5 slice) - reports in gpurun_out/, summarised with
+# tools/ncu_summary.py - then the full bench lines.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 timeout 120 python tools/c3_prof.py cfg3 2 > /dev/null || { echo "smoke hung"; exit 1; }
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_cfg3.csv $B --config cfg3 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"chain_(rows|carry|gemm)" -s 30 -c 3 -o gpurun_out/prof_cfg3 -f $B --config cfg3 > gpurun_out/ncu_cfg3.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused -s 3 -c 1 -o gpurun_out/prof_cfg5 -f $B --config cfg5 > gpurun_out/ncu_cfg5.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 30 --csv --log-file gpurun_out/launches_cfg5.csv $B --config cfg5 > /dev/null 2>&1
+for c in cfg3 cfg5; do
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_$c.csv python tools/c3_prof.py $c 4 > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"chain_(rows|carry|gemm)" -s 3 -c 3 -o gpurun_out/prof_$c -f python tools/c3_prof.py $c 3 > gpurun_out/ncu_$c.log 2>&1
+done
+timeout 400 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -1 gpurun_out/bench_default.json | cut -c1-300
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+for c in cfg1 cfg2 cfg4 cfg5; do
+  timeout 400 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+  python -c "import json; d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], d['value'], d['roofline']['frac'], d['e2e']['value'], d['parity_check']['max_abs_err_over_peak'])"
+done
 ls -la gpurun_out/*.ncu-rep

@@ -55,6 +55,9 @@ def main():
     launches = None
     if "--launches" in sys.argv:
         launches = sys.argv[sys.argv.index("--launches") + 1]
+    units = None  # channel-samples of the profiled call (when it is a slice of the bench config)
+    if "--units" in sys.argv:
+        units = float(sys.argv[sys.argv.index("--units") + 1])
     kernels = raw(report)
     md = [f"# {title}", "", f"report: `{os.path.basename(report)}` (ncu --set full --clock-control none)", ""]
     summary = {}
@@ -81,6 +84,9 @@ def main():
         # traffic and time are summed over the kernels of the report
         summary = {"kernel": " + ".join(names), "dram_bytes_per_launch": tot_bytes, "duration_us": tot_us,
                    "kernels_in_pass": len(names), "report": os.path.basename(report)}
+        if units:
+            summary["profiled_units"] = units
+            summary["dram_bytes_per_unit"] = tot_bytes / units
         if len(names) > 1:
             md.append(f"**pass total** ({len(names)} kernels): DRAM {tot_bytes:.4e} B, {tot_us:.1f} us (serialised, cold)")
             md.append("")
