@@ -494,3 +494,22 @@ def test_chain_pass_stopband_input_f64():
     y = wp.pipe(wp.Wave(x, fs), wp.Chain(stages)).samples
     ref = oracle.pipe(np.asarray(x, np.float32).astype(np.float64), wp.Chain(stages).bind(fs).stages)
     assert oracle.parity_error(y, ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+def test_multi_pass_chain_normalize_chain():
+    """chain pass -> Normalize -> chain pass: ping-pong buffers, workspace reuse
+    and the dependent launches of consecutive three-kernel passes."""
+    fs = 48000
+    stages = [wp.design_butterworth("hp", 4, 120, fs), wp.design_fir("lp", 33, 9000, fs=fs), wp.Normalize(0.8),
+              wp.design_chebyshev1("lp", 4, 1.0, 6000, fs), wp.design_fir("lp", 65, 12000, fs=fs), wp.Gain(0.5)]
+    rng = np.random.default_rng(41)
+    w = wp.Wave(rng.standard_normal((3, 50001)), fs)
+    from paper_2504_08624_b200 import engine
+
+    plan = engine.plan_for(wp.Chain(stages).bind(fs).stages, device=0)
+    desc = plan.describe_for(3, 50001)
+    assert len(desc) == 3 and "chain_gemm" in desc[0] and desc[1].startswith("normalize") and "chain_gemm" in desc[2]
+    y = wp.pipe(w, wp.Chain(stages)).samples
+    ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
