@@ -513,3 +513,39 @@ def test_multi_pass_chain_normalize_chain():
     y = wp.pipe(w, wp.Chain(stages)).samples
     ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
     assert oracle.parity_error(y, ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+def test_plan_execute_in_cuda_graph():
+    """plan.execute never allocates or synchronises, so a chain pass (three
+    kernels with dependent launches) can be captured once and replayed."""
+    import torch
+
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    bound = wp.Chain(_cfg3()).bind(fs).stages
+    plan = engine.plan_for(bound, device=0)
+    C, N = 4, 100003
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.standard_normal((C, N)).astype(np.float32)).cuda()
+    y_eager = torch.empty_like(x)
+    y_graph = torch.full_like(x, 3.0)
+    nb = plan.workspace_bytes(C, N)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.execute(x.data_ptr(), y_eager.data_ptr(), C, N, N, N, ws.data_ptr(), nb, s.cuda_stream)  # warm-up
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.execute(x.data_ptr(), y_graph.data_ptr(), C, N, N, N, ws.data_ptr(), nb,
+                     torch.cuda.current_stream().cuda_stream)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_graph, y_eager)
+    ref = oracle.pipe(x.double().cpu().numpy(), bound)
+    assert oracle.parity_error(y_graph.double().cpu().numpy(), ref) <= IIR_TOL
