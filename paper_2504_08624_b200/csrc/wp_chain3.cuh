@@ -95,7 +95,7 @@ struct C3GemmArgs {
     int dbg;                    // diagnostics: 4 = no state term
     unsigned long long *trace;  // optional: [tiles][C3_TRACE_EV] globaltimer stamps
 };
-constexpr int C3_TRACE_EV = 8;
+constexpr int C3_TRACE_EV = 10;
 
 namespace c3d {
 
@@ -605,7 +605,9 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                 const uint32_t par = (uint32_t)((i >> 1) & 1);
                 const int sa = i % C3_NA;
                 const uint32_t para = (uint32_t)((i / C3_NA) & 1);
+                C3TR(first + (long long)i * stride, 8);
                 wptc::mbar_wait(OPF(s), par);
+                C3TR(first + (long long)i * stride, 9);
                 wptc::mbar_wait(ACE(sa), para ^ 1u);
                 wptc::fence_after_sync();
                 C3TR(first + (long long)i * stride, 2);

@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_2504_08624_b200 as wp  # noqa: E402
 from paper_2504_08624_b200 import _native, engine  # noqa: E402
 
-EV = 8
+EV = 10
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 cfg = bench.CONFIGS[name]
 C, fs = cfg["C"], cfg["fs"]
@@ -38,9 +38,9 @@ _native.set_trace(0, 0)
 t = tr.view(tiles, EV).cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan)
-names = ["conv0", "opfull", "mma0", "mma1", "st0", "st1", "epi0", "epi1"]
+names = ["conv0", "opfull", "mma0", "mma1", "st0", "st1", "epi0", "epi1", "mmaTop", "mmaOPF"]
 print("gemm span us: %.1f" % (np.nanmax(t[:, 7]) / 1e3))
-for a, b in [(0, 1), (1, 2), (2, 3), (4, 5), (3, 5), (5, 6), (6, 7), (0, 7)]:
+for a, b in [(0, 1), (1, 2), (2, 3), (4, 5), (3, 5), (5, 6), (6, 7), (0, 7), (8, 9), (9, 2), (3, 8)]:
     d = (t[:, b] - t[:, a]) / 1e3
     print(f"{names[a]:>6} -> {names[b]:<6} median {np.nanmedian(d):7.2f} us  p90 {np.nanpercentile(d, 90):7.2f}")
 G = min(tiles, 148)
