@@ -21,7 +21,6 @@ import os
 import struct
 from dataclasses import dataclass
 
-import numpy as np
 
 from .errors import InvalidArgument, MalformedRiff, UnsupportedEncoding
 from .wave import Wave, _torch
@@ -58,27 +57,31 @@ def _encoding_of(tag: int, bits: int) -> str:
     raise UnsupportedEncoding(f"format tag {tag} with {bits} bits per sample is not supported")
 
 
-def _scan(data: bytes):
-    """Walk the RIFF chunks: (WavFormat, bits, data offset, data length)."""
-    if len(data) < 12:
+def _scan(fh, total: int):
+    """Walk the RIFF chunks of an open file (chunk headers and the fmt body
+    only): (WavFormat, bits, data offset, data length)."""
+    fh.seek(0)
+    head = fh.read(12)
+    if len(head) < 12:
         raise MalformedRiff("file shorter than a RIFF header")
-    magic, riff_size, form = struct.unpack_from("<4sI4s", data, 0)
+    magic, riff_size, form = struct.unpack_from("<4sI4s", head, 0)
     if magic != b"RIFF" or form != b"WAVE":
         raise MalformedRiff(f"not a RIFF/WAVE file (magic {magic!r}/{form!r})")
     end = 8 + riff_size
-    if end > len(data):
-        raise MalformedRiff(f"RIFF size {riff_size} exceeds file length {len(data)}")
+    if end > total:
+        raise MalformedRiff(f"RIFF size {riff_size} exceeds file length {total}")
     fmt = payload = None
     pos = 12
     while pos + 8 <= end:
-        cid, size = struct.unpack_from("<4sI", data, pos)
+        fh.seek(pos)
+        cid, size = struct.unpack("<4sI", fh.read(8))
         body = pos + 8
         if body + size > end:
             raise MalformedRiff(f"chunk {cid!r} of size {size} overruns the file")
         if cid == b"fmt ":
             if size < 16:
                 raise MalformedRiff(f"fmt chunk too short ({size} bytes)")
-            tag, channels, fs, _rate, block_align, bits = struct.unpack_from("<HHIIHH", data, body)
+            tag, channels, fs, _rate, block_align, bits = struct.unpack("<HHIIHH", fh.read(16))
             enc = _encoding_of(tag, bits)
             if channels < 1:
                 raise MalformedRiff("fmt chunk declares zero channels")
@@ -111,16 +114,20 @@ def load_wav(path, device=None) -> Wave:
 
     _require_cuda()
     with open(os.fspath(path), "rb") as fh:
-        data = fh.read()
-    try:
-        fmt, bits, off, size = _scan(data)
-    except struct.error as exc:
-        raise MalformedRiff(f"{path}: truncated chunk ({exc})") from None
-    C = fmt.channels
-    N = size // (C * bits // 8)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    host = torch.empty(size, dtype=torch.uint8, pin_memory=True)
-    host.numpy()[:] = np.frombuffer(data, dtype=np.uint8, count=size, offset=off)
+        # the header walk reads chunk headers only; the data chunk lands straight
+        # in pinned memory (no intermediate host copy)
+        total = os.fstat(fh.fileno()).st_size
+        try:
+            fmt, bits, off, size = _scan(fh, total)
+        except struct.error as exc:
+            raise MalformedRiff(f"{path}: truncated chunk ({exc})") from None
+        C = fmt.channels
+        N = size // (C * bits // 8)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        host = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        fh.seek(off)
+        if fh.readinto(memoryview(host.numpy())) != size:
+            raise MalformedRiff(f"{path}: data chunk shorter than declared")
     with torch.cuda.device(dev):
         raw = host.to(dev, non_blocking=True)
         out = torch.empty((C, N), dtype=torch.float32, device=dev)
@@ -160,6 +167,6 @@ def save_wav(wave: Wave, path, encoding: str = "float32") -> int:
         fh.write(struct.pack("<4sI4s", b"RIFF", riff_size, b"WAVE"))
         fh.write(fmt_chunk)
         fh.write(struct.pack("<4sI", b"data", nbytes))
-        fh.write(host.numpy().tobytes())
+        fh.write(memoryview(host.numpy()))
         fh.write(pad)
     return n_clip if encoding != "float32" else 0
