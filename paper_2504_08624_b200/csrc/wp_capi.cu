@@ -652,10 +652,11 @@ int finalize_pass(Pass &p) {
                 const float val = (t >= 0 && t < p.T) ? (float)std::ldexp(p.taps[t], f) : 0.f;
                 const __half hi = __float2half_rn(val);
                 const __half lo = __float2half_rn((val - __half2float(hi)) * 2048.f);
-                const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)pcol * 128u + (uint32_t)(k % 64) * 2u;
+                // [atom][hi rows 0..63 | lo rows 64..127][128 B]: one N = 128 operand per K atom
+                const uint32_t logical = (uint32_t)(k / 64) * 16384u + (uint32_t)pcol * 128u + (uint32_t)(k % 64) * 2u;
                 const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
                 img[phys / 2] = hi;
-                img[split + phys / 2] = lo;
+                img[(phys + 8192u) / 2] = lo;
             }
         cudaError_t e = cudaMalloc(&p.d_Bimg, img.size() * sizeof(__half));
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (lane == 0) {
-            const uint32_t idesc = wptc::idesc_f16(128, 64);
+            const uint32_t idesc = wptc::idesc_f16(128, 64), idesc2 = wptc::idesc_f16(128, 128);
             const uint32_t op0 = wptc::smem_u32(op), b0 = wptc::smem_u32(bimg);
             for (int i = 0; i < ntiles; ++i) {
                 const int s = i & 1;
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
 #pragma unroll 1
                 for (int kk = 0; kk < nk; ++kk) {
                     const uint64_t ka = 2u * kk;  // +32 B per K step (units of 16 B)
-                    const uint32_t boff = 8192u * (kk >> 2) + 32u * (kk & 3);
-                    const uint64_t bh = desc_sw128(b0 + boff), bl = desc_sw128(b0 + bBytes + boff);
-                    wptc::mma_f16(dm, ah0 + ka, bh, idesc, kk > 0);
-                    wptc::mma_f16(dc, al0 + ka, bh, idesc, kk > 0);
-                    wptc::mma_f16(dc, ah0 + ka, bl, idesc, 1u);
+                    // B image [atom][hi rows | lo rows x 2^11]: one N = 128 MMA puts
+                    // hi.hi into columns [0, 64) and hi.lo into [64, 128) = dc
+                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
+                    wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
+                    wptc::mma_f16(dc, al0 + ka, bb, idesc, 1u);
                 }
                 wptc::mma_commit(BAR(OP_EMPTY, s));
                 wptc::mma_commit(BAR(ACC_FULL, s));
