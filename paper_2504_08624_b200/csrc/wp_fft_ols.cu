@@ -122,6 +122,28 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         const bool has1 = c1 < a.C;
         const long long s = blk * a.L - a.Tpad;  // window start sample
         const float *x0 = a.x + c0 * a.ldx, *x1 = a.x + (has1 ? c1 : c0) * a.ldx;
+        if (t == 0) {
+            // warm L2 with the next work item's windows while this block is transformed
+            const long long nw = w + gridDim.x;
+            if (nw < a.total) {
+                const long long npair = nw / a.nblk, nblk = nw - npair * a.nblk;
+                const long long ns = nblk * a.L - a.Tpad;
+                long long lo = ns > 0 ? ns : 0, hi = ns + FM;
+                if (hi > a.N) hi = a.N;
+                lo &= ~3LL;
+                hi &= ~3LL;
+                if (hi > lo && (a.ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
+                    const uint32_t bytes = (uint32_t)(4 * (hi - lo));
+                    const long long nc0 = 2 * npair, nc1 = nc0 + 1;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + nc0 * a.ldx + lo), "r"(bytes)
+                                 : "memory");
+                    if (nc1 < a.C)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + nc1 * a.ldx + lo),
+                                     "r"(bytes)
+                                     : "memory");
+                }
+            }
+        }
         float2 v[32];
         const bool interior = s >= 0 && s + FM <= a.N;
         if (interior) {
