@@ -239,6 +239,7 @@ struct Pass {
     double ct_kscale[8] = {0};
     // decoupled tensor-core chain (rows -> carry -> gemm kernels)
     bool chain3 = false;
+    int c3_nop = 2;                   // fp16 operand stages of chain_gemm
     unsigned char *d_Eimg = nullptr;  // tf32 parts of the state-term matrix E
     double c3_st_scale = 1.0;
     // IIR-only passes keep the fused kernel for small calls and switch to the
@@ -461,7 +462,9 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
         p.c3_st_scale = std::ldexp(1.0, fB);
         p.chain3 = true;
         p.chain_tc = false;
-        smem = wp::chain3_smem_bytes(W, K, S, f64);
+        // a third operand stage when it fits (K = 64 IIR-only passes; not cfg3's K = 176)
+        p.c3_nop = wp::chain3_smem_bytes(W, K, S, f64, 3) <= 227 * 1024 ? 3 : 2;
+        smem = wp::chain3_smem_bytes(W, K, S, f64, p.c3_nop);
     }
     p.f64 = f64;
     p.ct_H = H;
@@ -474,8 +477,8 @@ int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
     if (p.chain3)
         snprintf(buf, sizeof buf,
                  "chain_rows+chain_carry+chain_gemm[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3+tf32x6 M128xN64 "
-                 "K=%d halo=%d tile=%d smem=%zu",
-                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
+                 "K=%d halo=%d tile=%d stages=%d smem=%zu",
+                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, p.c3_nop, smem);
     else
         snprintf(buf, sizeof buf,
                  "chain_tc[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3 M128xN64 K=%d halo=%d tile=%d smem=%zu",
@@ -584,7 +587,7 @@ int finalize_pass(Pass &p) {
         for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
         const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
         const int W = wpk::CT_TOUT, K = 64;
-        const size_t smem = wp::chain3_smem_bytes(W, K, p.S, f64);
+        const size_t smem = wp::chain3_smem_bytes(W, K, p.S, f64, 2);
         if (smem <= 227 * 1024) {
             Pass q = p;
             int rc = build_chain_tc(q, 0, K, W, f64, smem);
@@ -601,6 +604,7 @@ int finalize_pass(Pass &p) {
             p.c3_st_scale = q.c3_st_scale;
             p.ct_E = q.ct_E;
             p.c3_smem = q.smem;
+            p.c3_nop = q.c3_nop;
             p.c3_grid_cap = q.grid_cap;
             p.c3_desc = q.desc;
             p.c3_large = true;
@@ -621,7 +625,7 @@ int finalize_pass(Pass &p) {
         for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
         const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
         const size_t smem = chain_single_kernel() ? wp::chain_tc_smem_bytes(W, K, p.S, f64)
-                                                  : wp::chain3_smem_bytes(W, K, p.S, f64);
+                                                  : wp::chain3_smem_bytes(W, K, p.S, f64, 2);
         const int qcap = chain_single_kernel() ? wpk::CT_QMAX * wpk::CT_CONV : wpk::C3_QMAX * wpk::C3_CONV;
         if (W / 4 <= qcap && smem <= 227 * 1024) {
             int rc = build_chain_tc(p, H, K, W, f64, smem);
@@ -1076,6 +1080,7 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             g.trace = (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV) ? g_trace : nullptr;
             L.gemm_grid = (int)std::min<long long>(tiles, p.chain3 ? p.grid_cap : p.c3_grid_cap);
             L.smem = p.chain3 ? p.smem : p.c3_smem;
+            L.nop = p.c3_nop;
             e = wp::launch_chain3(p.f64, p.S, L, p.tables, stream);
             if (e != cudaSuccess) return cuda_fail(e, "chain3 launch");
         } else if (p.chain_tc) {

@@ -39,6 +39,7 @@ wpk::C3RowsTables<TS, 2 * S> c3_rows_tables(const HostTables &t) {
 
 template <typename TS, int S>
 cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream_t st) {
+    static_assert(sizeof(TS) >= 4, "scan dtype");
     constexpr int D = 2 * S;
     const wpk::C3RowsTables<TS, D> tb = c3_rows_tables<TS, S>(t);
     // chain_rows: persistent, as many CTAs as fit
@@ -90,7 +91,7 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // chain_gemm: one CTA per SM
-    auto kern = wpk::chain_gemm_kernel<TS, S>;
+    auto kern = L.nop == 3 ? wpk::chain_gemm_kernel<TS, S, 3> : wpk::chain_gemm_kernel<TS, S, 2>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
     {
@@ -121,7 +122,9 @@ cudaError_t c3_dispatch(int S, const Chain3Launch &L, const HostTables &t, cudaS
 
 }  // namespace
 
-size_t chain3_smem_bytes(int W, int K, int S, bool f64) { return wpk::C3Layout(W, K, 2 * S, f64 ? 8 : 4).total; }
+size_t chain3_smem_bytes(int W, int K, int S, bool f64, int nop) {
+    return wpk::C3Layout(W, K, 2 * S, f64 ? 8 : 4, nop).total;
+}
 
 cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st) {
     return f64 ? c3_dispatch<double>(S, L, t, st) : c3_dispatch<float>(S, L, t, st);

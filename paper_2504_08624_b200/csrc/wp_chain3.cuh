@@ -504,32 +504,33 @@ struct C3Layout {
     uint32_t rawBytes;
     uint32_t bimg, eimg, op, sop, raw, g, stg, misc, bars;
     uint32_t total;
-    __host__ __device__ C3Layout(int W, int K, int D, int ts) {
+    __host__ __device__ C3Layout(int W, int K, int D, int ts, int nop) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
         bBytes = (uint32_t)((K + 63) / 64) * 8192u;  // one part; the image is [atom][hi rows | lo rows]
         bimg = 0;
         eimg = bimg + 2 * bBytes;
         op = eimg + 3 * 2048u;
-        sop = op + 4 * opBytes;             // [2 stages][hi, lo]
+        sop = op + 2u * (uint32_t)nop * opBytes;  // op: [nop stages][hi, lo]
         raw = sop + 2u * 3u * 4096u;        // sop: [2 stages][3 parts][128 rows x 32 B]
         rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         g = raw + rawBytes;                 // raw: one fp32 window (bulk copy)
         stg = (g + (uint32_t)(ts * lt_size(D) * 32) + 15u) & ~15u;
         misc = stg + 4u * 32u * CT_STG_PITCH;  // scl[8] f32, red[8] f32, stag[8] i32
         bars = (misc + 96u + 15u) & ~15u;
-        total = bars + 24 * 8 + 16 + 1024;  // + alignment slack
+        total = bars + 20 * 8 + 16 + 1024;  // + alignment slack
     }
 };
 
-template <typename TS, int S>
+template <typename TS, int S, int NOP>
 __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmArgs a) {
+    static_assert(NOP == 2 || NOP == 3, "two or three fp16 operand stages");
     constexpr int D = 2 * S;
     static_assert(D <= 8, "state operand holds K = 8 columns");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nk = a.K / 16;
-    const C3Layout lay(a.W, a.K, D, (int)sizeof(TS));
+    const C3Layout lay(a.W, a.K, D, (int)sizeof(TS), NOP);
 #define C3TR(tile, ev) \
     do {                                                                              \
         if (a.trace) a.trace[(long long)(tile) * C3_TRACE_EV + (ev)] = ctd::gtimer(); \
@@ -543,23 +544,25 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
     float *red = scl + 8;                                     // [8]
     int *stag = reinterpret_cast<int *>(red + 8);             // [8] local tile index of scl[]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 20);
     const uint32_t bar0 = wptc::smem_u32(bars);
     // barriers: OP_FULL, OP_EMPTY, SOP_FULL, SOP_EMPTY x 2 stages; ACC_FULL, ACC_EMPTY x 4 stages
 #define OPF(s) (bar0 + 8u * (uint32_t)(0 + (s)))
-#define OPE(s) (bar0 + 8u * (uint32_t)(2 + (s)))
-#define SOF(s) (bar0 + 8u * (uint32_t)(4 + (s)))
-#define SOE(s) (bar0 + 8u * (uint32_t)(6 + (s)))
-#define ACF(s) (bar0 + 8u * (uint32_t)(8 + (s)))
-#define ACE(s) (bar0 + 8u * (uint32_t)(12 + (s)))
-#define RWF (bar0 + 8u * 16u)
-#define RWE (bar0 + 8u * 17u)
+#define OPE(s) (bar0 + 8u * (uint32_t)(3 + (s)))
+#define SOF(s) (bar0 + 8u * (uint32_t)(6 + (s)))
+#define SOE(s) (bar0 + 8u * (uint32_t)(8 + (s)))
+#define ACF(s) (bar0 + 8u * (uint32_t)(10 + (s)))
+#define ACE(s) (bar0 + 8u * (uint32_t)(14 + (s)))
+#define RWF (bar0 + 8u * 18u)
+#define RWE (bar0 + 8u * 19u)
 
     if (warp == 0) wptc::tmem_alloc(wptc::smem_u32(tmem_slot), 128 * C3_NA);
     if (tid == 32) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NOP; ++s) {
             wptc::mbar_init(OPF(s), 1);
             wptc::mbar_init(OPE(s), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             wptc::mbar_init(SOF(s), CT_ROWS);
             wptc::mbar_init(SOE(s), 1);
         }
@@ -601,19 +604,21 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
             const uint32_t op0 = wptc::smem_u32(op), b0 = wptc::smem_u32(bimg);
             const uint32_t sop0 = wptc::smem_u32(sop), e0 = wptc::smem_u32(smem + lay.eimg);
             for (int i = 0; i < ntiles; ++i) {
-                const int s = i & 1;
+                const int s = i & 1;  // state operand stage
                 const uint32_t par = (uint32_t)((i >> 1) & 1);
+                const int so = i % NOP;  // fp16 operand stage
+                const uint32_t paro = (uint32_t)((i / NOP) & 1);
                 const int sa = i % C3_NA;
                 const uint32_t para = (uint32_t)((i / C3_NA) & 1);
                 C3TR(first + (long long)i * stride, 8);
-                wptc::mbar_wait(OPF(s), par);
+                wptc::mbar_wait(OPF(so), paro);
                 C3TR(first + (long long)i * stride, 9);
                 wptc::mbar_wait(ACE(sa), para ^ 1u);
                 wptc::fence_after_sync();
                 C3TR(first + (long long)i * stride, 2);
                 // columns [0, 64): x_hi g_hi + x_lo g_hi (+ state term); [64, 128): x_hi g_lo
                 const uint32_t dm = tmem + 128u * sa;
-                const uint32_t ahi = op0 + (2u * s) * lay.opBytes, alo = ahi + lay.opBytes;
+                const uint32_t ahi = op0 + (2u * so) * lay.opBytes, alo = ahi + lay.opBytes;
                 const uint64_t ah0 = ctd::desc_sw128(ahi), al0 = ctd::desc_sw128(alo);
 #pragma unroll 1
                 for (int kk = 0; kk < nk; ++kk) {
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                     wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
                     wptc::mma_f16(dm, al0 + ka, bb, idesc, 1u);
                 }
-                wptc::mma_commit(OPE(s));  // the operand stage is free once the main GEMM has read it
+                wptc::mma_commit(OPE(so));  // the operand stage is free once the main GEMM has read it
                 C3TR(first + (long long)i * stride, 3);
                 wptc::mbar_wait(SOF(s), par);
                 wptc::fence_after_sync();
@@ -637,9 +642,6 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
                                       c3d::desc32(e0 + (uint32_t)ib * 2048u), idt);
                     }
                 }
-                // OPE only after SOF: the state role reads the tile's scale after
-                // waiting on OPF(s), so the converters must not complete the next
-                // OPF(s) phase before that wait (parity aliasing)
                 wptc::mma_commit(SOE(s));
                 wptc::mma_commit(ACF(sa));
             }
@@ -680,8 +682,8 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chain_gemm_kernel(const C3GemmA
         const int nq = a.W / 4;
         const float4 *raw4 = reinterpret_cast<const float4 *>(smem + lay.raw);
         for (int i = 0; i < ntiles; ++i) {
-            const int s = i & 1;
-            const uint32_t par = (uint32_t)((i >> 1) & 1);
+            const int s = i % NOP;
+            const uint32_t par = (uint32_t)((i / NOP) & 1);
             const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
             const float *xr = a.x + g.c * a.ldx;
             const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;

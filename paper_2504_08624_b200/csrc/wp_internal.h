@@ -98,8 +98,9 @@ struct Chain3Launch {
     std::vector<double> carry_mats;  // [7][D][D]: MT = M^32, MT^(B 2^i) i < 5, MT^(32 B)
     int gemm_grid = 1;
     size_t smem = 0;
+    int nop = 2;  // fp16 operand stages of chain_gemm (3 when they fit next to the rest)
 };
-size_t chain3_smem_bytes(int W, int K, int S, bool f64);
+size_t chain3_smem_bytes(int W, int K, int S, bool f64, int nop);
 cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st);
 
 // WAV payload codec (wp_wav.cu)
