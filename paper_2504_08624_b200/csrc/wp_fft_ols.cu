@@ -208,14 +208,31 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         float *y0 = a.y + c0 * a.ldy, *y1 = a.y + (has1 ? c1 : c0) * a.ldy;
         const long long o0 = blk * a.L - a.Tpad;  // output index of window position 0
         float *q0 = y0 + o0 + t, *q1 = y1 + o0 + t;
-        const long long lim = a.N - o0 - t;  // valid while 512 j < lim
+        const int j0 = a.Tpad >> 9;  // Tpad is a multiple of 512: n = t + 512 j >= Tpad <=> j >= j0
+        if (o0 + FM <= a.N) {
+            // whole block inside the signal: no per-element bound (the common case)
+            if (has1) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int n = t + 512 * j;
-            if (n >= a.Tpad && 512LL * j < lim) {
-                const float2 r = v[brev(j, 5)];
-                __stcs(q0 + 512 * j, r.x);
-                if (has1) __stcs(q1 + 512 * j, r.y);
+                for (int j = 0; j < 32; ++j)
+                    if (j >= j0) {
+                        const float2 r = v[brev(j, 5)];
+                        __stcs(q0 + 512 * j, r.x);
+                        __stcs(q1 + 512 * j, r.y);
+                    }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j >= j0) __stcs(q0 + 512 * j, v[brev(j, 5)].x);
+            }
+        } else {
+            const long long lim = a.N - o0 - t;  // valid while 512 j < lim
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j >= j0 && 512LL * j < lim) {
+                    const float2 r = v[brev(j, 5)];
+                    __stcs(q0 + 512 * j, r.x);
+                    if (has1) __stcs(q1 + 512 * j, r.y);
+                }
             }
         }
     }
