@@ -1037,7 +1037,9 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             const int vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
             L.rows = wpk::C3RowsArgs{in, C, N, ld_in, tiles, p.ct_H, vec_x, p.d_G, rows, aggs};
             const int B = (int)((T + wpk::C3_CARRY_THREADS - 1) / wpk::C3_CARRY_THREADS);
-            L.carry = wpk::C3CarryArgs{C, T, B, aggs, carry};
+            L.carry = wpk::C3CarryArgs{C, T, B, nullptr, aggs, carry};
+            if (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV + (size_t)C * 8)
+                L.carry.trace = g_trace + (size_t)tiles * wpk::C3_TRACE_EV;
             {
                 // tile transfer M^128; thread-block and warp powers
                 const Mat &MT = p.tables.MT;

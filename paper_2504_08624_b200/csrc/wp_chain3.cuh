@@ -66,6 +66,7 @@ struct C3RowsTables {
 struct C3CarryArgs {
     long long C, T;  // channels, tiles per channel
     int B;           // tiles per thread
+    unsigned long long *trace;  // optional: [C][8] globaltimer stamps of thread 255
     const void *aggs;
     void *carry;     // [tiles][4][D] TS: state entering rows 0, 32, 64, 96 of each tile
 };
@@ -396,8 +397,13 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
     const TS *aggs = reinterpret_cast<const TS *>(a.aggs);
     TS *carry = reinterpret_cast<TS *>(a.carry);
     auto seg = [&](long long j) { return (size_t)(j * a.C + c) * D; };
+    auto stamp = [&](int ev) {
+        if (a.trace && tid == C3_CARRY_THREADS - 1) a.trace[c * 8 + ev] = ctd::gtimer();
+    };
+    stamp(0);
     c3d::pdl_trigger();  // chain_gemm may start its main GEMMs
     c3d::pdl_wait();     // chain_rows' aggregates are complete
+    stamp(1);
     auto mt = [&](int r, int q) { return tb.MT[r][q]; };
     // local inclusive prefix of this thread's segments (zero carry)
     TS loc[D];
@@ -417,6 +423,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
             for (int d = 0; d < D; ++d) loc[d] = cur[d];
         }
     }
+    stamp(2);
     // warp scan over threads (blocks of exactly B segments before any short one)
     TS incl[D];
 #pragma unroll
@@ -434,6 +441,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
         for (int d = 0; d < D; ++d) wt[wq][d] = incl[d];
     }
     __syncthreads();
+    stamp(3);
     TS ex[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
 #pragma unroll
         for (int d = 0; d < D; ++d) ex[d] += wc[d];
     }
+    stamp(4);
     // replay: carry of each owned segment
     {
         TS nxt[D];
@@ -495,6 +504,7 @@ __global__ void __launch_bounds__(C3_CARRY_THREADS) chain_carry_kernel(const C3C
             for (int d = 0; d < D; ++d) ex[d] = cur[d];
         }
     }
+    stamp(5);
 }
 
 // ---------------------------------------------------------------------------

@@ -27,7 +27,7 @@ nb = plan.workspace_bytes(C, N)
 ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 tiles = C * ((N + 8191) // 8192)
-tr = torch.zeros(tiles * EV, dtype=torch.int64, device="cuda")
+tr = torch.zeros(tiles * EV + C * 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
     plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
 torch.cuda.synchronize()
@@ -35,7 +35,13 @@ _native.set_trace(tr.data_ptr(), tr.numel())
 plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
 torch.cuda.synchronize()
 _native.set_trace(0, 0)
-t = tr.view(tiles, EV).cpu().numpy().astype(np.float64)
+all_t = tr.cpu().numpy().astype(np.float64)
+ct = all_t[tiles * EV:].reshape(C, 8)
+if (ct[:, 0] > 0).any():
+    d = np.diff(ct[:, :6], axis=1) / 1e3
+    print("chain_carry per-CTA phases (us, median): pdl_wait %.2f  local %.2f  scan %.2f  horner+pow %.2f  replay %.2f  total %.2f"
+          % tuple(list(np.median(d, axis=0)) + [np.median((ct[:, 5] - ct[:, 0]) / 1e3)]))
+t = all_t[:tiles * EV].reshape(tiles, EV)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan)
 names = ["conv0", "opfull", "mma0", "mma1", "st0", "st1", "epi0", "epi1", "mmaTop", "mmaOPF"]
