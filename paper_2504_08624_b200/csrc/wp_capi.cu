@@ -265,16 +265,18 @@ namespace wp {
 void count_launch(int n) { g_launches.fetch_add((unsigned long long)n); }
 
 int sm_count() {
-    static int cached[64] = {0};
+    static std::atomic<int> cached[64];  // per device; benign races write the same value
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) dev = 0;
-    if (!cached[dev]) {
+    int v = cached[dev].load(std::memory_order_relaxed);
+    if (!v) {
         int n = 0;
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        cached[dev] = n > 0 ? n : 1;
+        v = n > 0 ? n : 1;
+        cached[dev].store(v, std::memory_order_relaxed);
     }
-    return cached[dev];
+    return v;
 }
 
 }  // namespace wp

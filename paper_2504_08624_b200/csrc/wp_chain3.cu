@@ -1,6 +1,7 @@
 // Instantiations and launchers of the decoupled tensor-core chain
 // (wp_chain3.cuh): scan dtype float64 or float32, 1..4 SOS sections.
 #include <algorithm>
+#include <atomic>
 
 #include "wp_chain3.cuh"
 #include "wp_internal.h"
@@ -43,21 +44,22 @@ cudaError_t c3_launch_one(const Chain3Launch &L, const HostTables &t, cudaStream
     constexpr int D = 2 * S;
     const wpk::C3RowsTables<TS, D> tb = c3_rows_tables<TS, S>(t);
     // chain_rows: persistent, as many CTAs as fit
-    static int rows_occ[64] = {0};
+    static std::atomic<int> rows_occ[64];  // per device; benign races write the same value
     int dev = 0;
     cudaGetDevice(&dev);
     dev = dev < 0 || dev >= 64 ? 0 : dev;
     cudaError_t e = cudaFuncSetAttribute(wpk::chain_rows_kernel<TS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          wpk::c3_rows_smem<TS>());
     if (e != cudaSuccess) return e;
-    if (!rows_occ[dev]) {
+    if (!rows_occ[dev].load(std::memory_order_relaxed)) {
         int occ = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wpk::chain_rows_kernel<TS, S>, wpk::C3_ROWS_THREADS,
                                                           wpk::c3_rows_smem<TS>());
         if (e != cudaSuccess) return e;
-        rows_occ[dev] = std::max(occ, 1);
+        rows_occ[dev].store(std::max(occ, 1), std::memory_order_relaxed);
     }
-    const long long rg = std::min<long long>(L.rows.total_tiles, (long long)rows_occ[dev] * sm_count());
+    const long long rg =
+        std::min<long long>(L.rows.total_tiles, (long long)rows_occ[dev].load(std::memory_order_relaxed) * sm_count());
     wpk::chain_rows_kernel<TS, S><<<(unsigned)rg, wpk::C3_ROWS_THREADS, wpk::c3_rows_smem<TS>(), st>>>(L.rows, tb);
     count_launch();
     e = cudaGetLastError();
