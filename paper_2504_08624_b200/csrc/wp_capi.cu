@@ -23,6 +23,7 @@
 
 #include "../../include/wavepipe_b200.h"
 #include "wp_internal.h"
+#include "wp_lb.cuh"
 
 namespace wp {
 int fused_occupancy_f32(int S, bool fir, size_t smem);
@@ -249,6 +250,12 @@ struct Pass {
     size_t c3_smem = 0;
     int c3_grid_cap = 0;
     std::string c3_desc;
+    // single-pass tensor-core chain with look-back (wp_lb.cuh): IIR [+ FIR] passes;
+    // IIR-only passes of <= 4 sections keep the fused kernel for small calls
+    bool lb = false, lb_large = false;
+    long long lb_min_tiles = 0;
+    double gain = 1.0;  // combined gain of an LTI pass (lti planner)
+    wp::LbPlan lbp;
     std::string desc;
     bool empty() const { return kind == FUSED && S == 0 && T == 0 && pre == 1.f && post.empty(); }
 };
@@ -303,6 +310,14 @@ bool chain_tc_forced() {
 bool chain_single_kernel() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
     return v && std::string(v) == "tc1";
+}
+
+// default: single-pass look-back chain; WP_CHAIN_IMPL=c3 / cuda / tc / tc1 select the
+// round-1 kernels for A/B comparisons
+bool lb_enabled() {
+    const char *v = std::getenv("WP_CHAIN_IMPL");
+    return !(v && (std::string(v) == "c3" || std::string(v) == "cuda" || std::string(v) == "tc" ||
+                   std::string(v) == "tc1"));
 }
 
 float tf32_round(double v) {
@@ -570,6 +585,29 @@ int finalize_pass(Pass &p) {
         p.desc = buf;
         return WP_OK;
     }
+    if (p.S > 0 && lb_enabled() && wp::lb_fits(p.S, p.T)) {
+        double gain = (double)p.pre;
+        for (float g : p.post) gain *= (double)g;
+        if (p.gain != 1.0) gain = p.gain;
+        std::string err;
+        const int rc = wp::lb_build(p.lbp, p.sos, p.S, p.T > 0 ? p.taps : std::vector<double>{}, gain, err);
+        if (rc != WP_OK) return fail(rc, err);
+        if (p.T > 1 || p.S > wpk::MAXS) {
+            p.lb = true;
+            p.desc = p.lbp.desc;
+            return WP_OK;
+        }
+        // IIR-only: small calls keep the fused chunked scan (one launch, exact
+        // per-chunk recurrence for the known-answer cases)
+        p.lb_large = true;
+        p.lb_min_tiles = 2LL * wp::sm_count();
+        if (p.T == 1) {
+            // a 1-tap FIR is a gain: the fused kernel takes it as a post gain
+            p.post.push_back((float)p.taps[0]);
+            p.T = 0;
+            p.taps.clear();
+        }
+    }
     if (p.S == 0 && p.T >= 8 && fir_tc_enabled()) {
         // tensor-core direct FIR: rows of 64 samples, K covers taps + 63 phases
         p.tc_Tp = (p.T - 1 + 7) / 8 * 8;
@@ -581,7 +619,7 @@ int finalize_pass(Pass &p) {
     // on the CUDA-core chunked scan, which measured faster for them (cfg5
     // slice 295 vs 254 G ch-s/s, cfg3's IIR part 0.97 vs 1.25 ms;
     // tools/iir_probe.py). WP_CHAIN_IMPL=tc forces the tensor-core kernel.
-    if (p.S > 0 && p.T == 0 && chain_tc_enabled() && !chain_tc_forced()) {
+    if (p.S > 0 && p.T == 0 && chain_tc_enabled() && !chain_tc_forced() && !p.lb_large) {
         // large IIR-only calls: the three-kernel chain beats the fused scan
         // (cfg5: 42.5 vs 47.7 ms); small ones keep the fused kernel (fewer
         // launches; exact per-chunk recurrence for the known-answer cases)
@@ -617,7 +655,7 @@ int finalize_pass(Pass &p) {
             if (q.d_Bk) cudaFree(q.d_Bk);
         }
     }
-    if (p.S > 0 && chain_tc_enabled() && (p.T > 1 || chain_tc_forced())) {
+    if (p.S > 0 && !p.lb_large && chain_tc_enabled() && (p.T > 1 || chain_tc_forced())) {
         const int T = p.T > 0 ? p.T : 1;
         const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
         const int K = H + 64;
@@ -736,10 +774,12 @@ int finalize_pass(Pass &p) {
              p.S ? (p.f64 ? "(f64)" : "(f32)") : "", p.T, p.post.size(), p.Lout, p.H, p.smem, occ);
     p.desc = buf;
     if (p.c3_large) p.desc += " ; from " + std::to_string(p.c3_min_tiles) + " tiles: " + p.c3_desc;
+    if (p.lb_large) p.desc += " ; from " + std::to_string(p.lb_min_tiles) + " tiles: " + p.lbp.desc;
     return WP_OK;
 }
 
 void free_pass(Pass &p) {
+    wp::lb_free(p.lbp);
     if (p.d_Bimg) cudaFree(p.d_Bimg);
     p.d_Bimg = nullptr;
     if (p.d_Bk) cudaFree(p.d_Bk);
@@ -766,6 +806,17 @@ size_t rec_bytes(const Pass &p) {
 }
 
 long long tiles_per_channel(const Pass &p, long long N) { return (N + p.Lout - 1) / p.Lout; }
+
+bool uses_lb(const Pass &p, long long C, long long N) {
+    return p.lb || (p.lb_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.lb_min_tiles);
+}
+
+// look-back records / scan buffers of one pass for a [C x N] call
+size_t pass_rec_bytes(const Pass &p, long long C, long long N) {
+    size_t b = rec_bytes(p) * (size_t)(tiles_per_channel(p, N) * C);
+    if (p.lb || p.lb_large) b = std::max(b, wp::lb_workspace_bytes(p.lbp, C, ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C));
+    return b;
+}
 
 int arch_ok() {
     static int cached = -99;
@@ -817,8 +868,74 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
         if (!cur.empty()) passes.push_back(cur);
         cur = Pass();
     };
+    const bool lti = lb_enabled();
     for (int si = 0; si < n_stages; ++si) {
         const wp_stage &st = stages[si];
+        if (lti) {
+            // LTI planner: every run of IIR / FIR / gain stages between
+            // Normalize stages is ONE linear time-invariant system, so its
+            // order does not matter (FIR -> IIR fuses like IIR -> FIR) and it
+            // runs as one pass while it fits the single-pass kernel (<= 8
+            // sections, FIR halo <= LB_MAX_H); a longer FIR gets its own pass.
+            const int lbh = wpk::LB_MAX_H;
+            if (st.kind == WP_STAGE_GAIN) {
+                if (!std::isfinite(st.value)) {
+                    delete plan;
+                    return fail(WP_EINVAL, "gain must be finite");
+                }
+                cur.gain *= st.value;
+                cur.pre = (float)cur.gain;
+                continue;
+            }
+            if (st.kind == WP_STAGE_IIR) {
+                if (st.n < 1 || !st.coef) {
+                    delete plan;
+                    return fail(WP_EINVAL, "IIR stage needs >= 1 section");
+                }
+                std::vector<int> keep;
+                for (int k = 0; k < st.n; ++k) {
+                    const double *r = st.coef + 5 * k;
+                    if (!(r[0] == 1.0 && r[1] == 0.0 && r[2] == 0.0 && r[3] == 0.0 && r[4] == 0.0)) keep.push_back(k);
+                }
+                if (keep.empty()) continue;
+                for (size_t idx = 0; idx < keep.size(); ++idx) {
+                    if (cur.S == 8 || (cur.T > 0 && cur.T - 1 > lbh)) close();
+                    for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * keep[idx] + j]);
+                    cur.S += 1;
+                    cur.prec_flag |= st.flags & (WP_IIR_PREC_F32 | WP_IIR_PREC_F64);
+                }
+                continue;
+            }
+            if (st.kind == WP_STAGE_FIR) {
+                if (st.n < 1 || !st.coef) {
+                    delete plan;
+                    return fail(WP_EINVAL, "FIR stage needs >= 1 tap");
+                }
+                const bool long_fir = st.n - 1 > lbh;
+                if (cur.T > 0) {
+                    const int comb = cur.T + st.n - 1;
+                    if (comb - 1 > lbh || long_fir) close();
+                } else if (long_fir && cur.S > 0) {
+                    close();
+                }
+                if (cur.T > 0) {
+                    // convolve with the pass's FIR (both causal, same-length truncation later)
+                    std::vector<long double> t((size_t)cur.T + st.n - 1, 0.0L);
+                    for (int a = 0; a < cur.T; ++a)
+                        for (int b = 0; b < st.n; ++b) t[a + b] += (long double)cur.taps[a] * (long double)st.coef[b];
+                    cur.taps.assign(t.size(), 0.0);
+                    for (size_t i = 0; i < t.size(); ++i) cur.taps[i] = (double)t[i];
+                    cur.T = (int)t.size();
+                    cur.fir_flags = 0;
+                } else {
+                    cur.T = st.n;
+                    cur.taps.assign(st.coef, st.coef + st.n);
+                    cur.fir_flags = st.flags & (WP_FIR_DIRECT | WP_FIR_FFT);
+                }
+                if (long_fir) close();  // a long FIR stays a FIR-only pass
+                continue;
+            }
+        }
         switch (st.kind) {
             case WP_STAGE_GAIN: {
                 if (!std::isfinite(st.value)) {
@@ -922,7 +1039,7 @@ int wp_plan_num_passes(const wp_plan *plan) { return plan ? (int)plan->passes.si
 int wp_plan_launches(const wp_plan *plan) {
     if (!plan) return 0;
     int n = 0;
-    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : p.chain3 ? 3 : 1;
+    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : p.lb ? 1 : p.chain3 ? 3 : 1;
     return n;
 }
 
@@ -933,13 +1050,16 @@ static bool uses_c3(const Pass &p, int64_t C, int64_t N) {
 int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames) {
     if (!plan) return 0;
     int n = 0;
-    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : uses_c3(p, channels, frames) ? 3 : 1;
+    for (const Pass &p : plan->passes)
+        n += p.kind != Pass::FUSED ? 2 : uses_lb(p, channels, frames) ? 1 : uses_c3(p, channels, frames) ? 3 : 1;
     return n;
 }
 
 const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t channels, int64_t frames) {
     if (!plan || pass < 0 || pass >= (int)plan->passes.size()) return "";
     const Pass &p = plan->passes[pass];
+    if (p.lb) return p.desc.c_str();
+    if (p.lb_large) return uses_lb(p, channels, frames) ? p.lbp.desc.c_str() : p.desc.c_str();
     if (p.c3_large) return uses_c3(p, channels, frames) ? p.c3_desc.c_str() : p.desc.c_str();
     return p.desc.c_str();
 }
@@ -951,7 +1071,7 @@ const char *wp_plan_describe(const wp_plan *plan, int32_t pass) {
 
 static size_t ws_layout(const wp_plan *plan, int64_t C, int64_t N, size_t *rec_off, size_t *tmp_off, int64_t *ld_tmp) {
     size_t recb = 0;
-    for (const Pass &p : plan->passes) recb = std::max(recb, rec_bytes(p) * (size_t)(tiles_per_channel(p, N) * C));
+    for (const Pass &p : plan->passes) recb = std::max(recb, pass_rec_bytes(p, C, N));
     *rec_off = 256;
     *tmp_off = (256 + recb + 255) / 256 * 256;
     *ld_tmp = (N + 63) / 64 * 64;
@@ -1008,6 +1128,12 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             if (e != cudaSuccess) return cuda_fail(e, "peak_abs launch");
             e = wp::launch_scale_by_peak(in, out, C, N, ld_in, ld_out, peak, (float)p.target, stream);
             if (e != cudaSuccess) return cuda_fail(e, "scale launch");
+        } else if (uses_lb(p, C, N)) {
+            const long long tiles = ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C;
+            if (tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
+            unsigned long long *tr = (g_trace && g_trace_entries >= (size_t)tiles * wpk::LB_TRACE_EV) ? g_trace : nullptr;
+            e = wp::lb_launch(p.lbp, in, out, C, N, ld_in, ld_out, ws + rec_off, tr, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "chain_lb launch");
         } else if (p.fft) {
             wpk::FftArgs a{};
             a.x = in;

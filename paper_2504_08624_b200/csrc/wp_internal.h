@@ -103,6 +103,26 @@ struct Chain3Launch {
 size_t chain3_smem_bytes(int W, int K, int S, bool f64, int nop);
 cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st);
 
+// single-pass tensor-core chain with look-back (wp_lb.cu / wp_lb.cuh)
+struct LbPlan {
+    int D = 0, H = 0, K = 0, W = 0, nop = 2;
+    size_t smem = 0;
+    unsigned char *d_bimg = nullptr;
+    float *d_stabs = nullptr, *d_MTl = nullptr;
+    float out_scale = 1.f;
+    float escale[16] = {};
+    std::string desc;
+};
+// S sections (<= 8) and T taps (T <= 1: no FIR) fit the kernel's shared memory
+bool lb_fits(int S, int T);
+size_t lb_smem_bytes(int D, int H, int nop);
+int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps, double gain,
+             std::string &err);
+void lb_free(LbPlan &p);
+size_t lb_workspace_bytes(const LbPlan &p, long long channels, long long tiles);
+cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, long long N, long long ldx, long long ldy,
+                      void *ws, unsigned long long *trace, cudaStream_t st);
+
 // WAV payload codec (wp_wav.cu)
 cudaError_t launch_wav_decode(const void *payload, int enc, float *y, long long C, long long N, long long ld,
                               cudaStream_t st);

@@ -1,0 +1,516 @@
+// Host side of the single-pass tensor-core chain (wp_lb.cuh): per-section
+// balanced state basis, plan-time tables, launcher.
+//
+// Why a balanced basis: the reference's DF2T states (_kernels_jit.py:27-32)
+// of a section with poles near z = 1 (cfg3's 100 Hz high-pass, r = 0.995) are
+// large and nearly cancel, so a scan over them needs fp64 (round 1). After
+// the similarity transform s -> T s that balances each section's
+// controllability and observability Gramians, the same input/output map has
+// well-scaled states, and an fp32 scan + fp32 state term stays within
+// ~3e-5 of the fp64 reference even for a 3 Hz sine into a 100 Hz high-pass
+// (tools/balance_probe.py).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/wavepipe_b200.h"
+#include "wp_internal.h"
+#include "wp_lb.cuh"
+
+namespace wp {
+
+namespace {
+
+using LD = long double;
+using MatL = std::vector<LD>;  // row-major n x n
+
+MatL mat_mul(const MatL &a, const MatL &b, int n) {
+    MatL c((size_t)n * n, 0.0L);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) {
+            const LD v = a[i * n + k];
+            if (v == 0.0L) continue;
+            for (int j = 0; j < n; ++j) c[i * n + j] += v * b[k * n + j];
+        }
+    return c;
+}
+
+MatL mat_eye(int n) {
+    MatL m((size_t)n * n, 0.0L);
+    for (int i = 0; i < n; ++i) m[i * n + i] = 1.0L;
+    return m;
+}
+
+MatL mat_pow(const MatL &m, long long e, int n) {
+    MatL r = mat_eye(n), b = m;
+    while (e > 0) {
+        if (e & 1) r = mat_mul(r, b, n);
+        b = mat_mul(b, b, n);
+        e >>= 1;
+    }
+    return r;
+}
+
+// Solve W - A W A^T = Q for 2x2 (Kronecker form, Gaussian elimination).
+bool lyap2(const LD A[4], const LD Q[4], LD W[4]) {
+    LD M[4][5];
+    for (int r = 0; r < 4; ++r) {
+        const int i = r / 2, j = r % 2;
+        for (int c = 0; c < 4; ++c) {
+            const int k = c / 2, l = c % 2;
+            M[r][c] = (r == c ? 1.0L : 0.0L) - A[i * 2 + k] * A[j * 2 + l];
+        }
+        M[r][4] = Q[r];
+    }
+    for (int c = 0; c < 4; ++c) {
+        int p = c;
+        for (int r = c + 1; r < 4; ++r)
+            if (std::fabs(M[r][c]) > std::fabs(M[p][c])) p = r;
+        if (std::fabs(M[p][c]) < 1e-300L) return false;
+        for (int k = 0; k < 5; ++k) std::swap(M[c][k], M[p][k]);
+        for (int r = 0; r < 4; ++r) {
+            if (r == c) continue;
+            const LD f = M[r][c] / M[c][c];
+            for (int k = c; k < 5; ++k) M[r][k] -= f * M[c][k];
+        }
+    }
+    for (int r = 0; r < 4; ++r) W[r] = M[r][4] / M[r][r];
+    return true;
+}
+
+// symmetric 2x2 eigen-decomposition: W = U diag(l) U^T (columns of U)
+void eig2(const LD W[4], LD l[2], LD U[4]) {
+    const LD a = W[0], b = 0.5L * (W[1] + W[2]), d = W[3];
+    if (std::fabs(b) < 1e-300L) {
+        l[0] = a, l[1] = d;
+        U[0] = 1, U[1] = 0, U[2] = 0, U[3] = 1;
+        return;
+    }
+    const LD th = 0.5L * std::atan2(2.0L * b, a - d);
+    const LD c = std::cos(th), s = std::sin(th);
+    l[0] = c * c * a + 2 * c * s * b + s * s * d;
+    l[1] = s * s * a - 2 * c * s * b + c * c * d;
+    U[0] = c, U[1] = -s, U[2] = s, U[3] = c;  // columns (c, s), (-s, c)
+}
+
+// L with W ~= L L^T, eigenvalues clamped to >= eps * max (non-minimal sections)
+void psd_factor2(const LD W[4], LD L[4]) {
+    LD l[2], U[4];
+    eig2(W, l, U);
+    const LD mx = std::max(std::max(l[0], l[1]), (LD)1e-300L);
+    for (int j = 0; j < 2; ++j) {
+        const LD v = std::sqrt(std::max(l[j], 1e-12L * mx));
+        L[0 * 2 + j] = U[0 * 2 + j] * v;
+        L[1 * 2 + j] = U[1 * 2 + j] * v;
+    }
+}
+
+// T (2x2) and its inverse balancing one DF2T section; false -> keep identity
+bool balance_section(const double *sec, LD T[4], LD Ti[4]) {
+    const LD b0 = sec[0], b1 = sec[1], b2 = sec[2], a1 = sec[3], a2 = sec[4];
+    const LD A[4] = {-a1, 1.0L, -a2, 0.0L};
+    const LD B[2] = {b1 - a1 * b0, b2 - a2 * b0};
+    const LD At[4] = {A[0], A[2], A[1], A[3]};
+    const LD Qc[4] = {B[0] * B[0], B[0] * B[1], B[1] * B[0], B[1] * B[1]};
+    const LD Qo[4] = {1.0L, 0.0L, 0.0L, 0.0L};  // C = (1, 0)
+    LD Wc[4], Wo[4];
+    if (!lyap2(A, Qc, Wc) || !lyap2(At, Qo, Wo)) return false;
+    LD Lc[4], Lo[4];
+    psd_factor2(Wc, Lc);
+    psd_factor2(Wo, Lo);
+    // X = Lo^T Lc = U S V^T
+    LD X[4];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) X[i * 2 + j] = Lo[0 * 2 + i] * Lc[0 * 2 + j] + Lo[1 * 2 + i] * Lc[1 * 2 + j];
+    LD XtX[4];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) XtX[i * 2 + j] = X[0 * 2 + i] * X[0 * 2 + j] + X[1 * 2 + i] * X[1 * 2 + j];
+    LD s2[2], V[4];
+    eig2(XtX, s2, V);
+    LD S[2], U[4];
+    for (int j = 0; j < 2; ++j) {
+        S[j] = std::sqrt(std::max(s2[j], (LD)0));
+        if (!(S[j] > 0)) return false;
+        // U[:, j] = X V[:, j] / S[j]
+        U[0 * 2 + j] = (X[0] * V[0 * 2 + j] + X[1] * V[1 * 2 + j]) / S[j];
+        U[1 * 2 + j] = (X[2] * V[0 * 2 + j] + X[3] * V[1 * 2 + j]) / S[j];
+    }
+    // T = S^-1/2 U^T Lo^T ; Ti = Lc V S^-1/2
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            const LD si = 1.0L / std::sqrt(S[i]), sj = 1.0L / std::sqrt(S[j]);
+            T[i * 2 + j] = si * (U[0 * 2 + i] * Lo[j * 2 + 0] + U[1 * 2 + i] * Lo[j * 2 + 1]);
+            Ti[i * 2 + j] = (Lc[i * 2 + 0] * V[0 * 2 + j] + Lc[i * 2 + 1] * V[1 * 2 + j]) * sj;
+        }
+    // sanity: T Ti = I
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            const LD v = T[i * 2 + 0] * Ti[0 * 2 + j] + T[i * 2 + 1] * Ti[1 * 2 + j];
+            if (!std::isfinite((double)v) || std::fabs(v - (i == j ? 1.0L : 0.0L)) > 1e-9L) return false;
+        }
+    return true;
+}
+
+// DF2T cascade state space (states w1, w2 per section, section-major)
+void cascade_df2t(const std::vector<double> &sos, int S, MatL &A, std::vector<LD> &B, std::vector<LD> &C, LD &d) {
+    const int D = 2 * S;
+    A.assign((size_t)D * D, 0.0L);
+    B.assign(D, 0.0L);
+    C.assign(D, 0.0L);
+    auto step = [&](const std::vector<LD> &st, LD u, std::vector<LD> &out) -> LD {
+        for (int s = 0; s < S; ++s) {
+            const LD b0 = sos[5 * s], b1 = sos[5 * s + 1], b2 = sos[5 * s + 2], a1 = sos[5 * s + 3], a2 = sos[5 * s + 4];
+            const LD y = b0 * u + st[2 * s];
+            out[2 * s] = b1 * u - a1 * y + st[2 * s + 1];
+            out[2 * s + 1] = b2 * u - a2 * y;
+            u = y;
+        }
+        return u;
+    };
+    std::vector<LD> e(D), o(D);
+    for (int j = 0; j < D; ++j) {
+        std::fill(e.begin(), e.end(), 0.0L);
+        e[j] = 1.0L;
+        C[j] = step(e, 0.0L, o);
+        for (int i = 0; i < D; ++i) A[i * D + j] = o[i];
+    }
+    std::fill(e.begin(), e.end(), 0.0L);
+    d = step(e, 1.0L, B);
+}
+
+void put_lt(float *dst, const MatL &m, int D) {
+    for (int r = 0; r < D; ++r)
+        for (int q = 0; q < wpk::lt_nj(r); ++q) dst[wpk::lt_off(r) + q] = (float)m[r * D + q];
+}
+
+int exp_of(double v) {
+    int ex = 0;
+    if (v > 0) std::frexp(v, &ex);
+    return ex;
+}
+
+template <int D, int NOP>
+cudaError_t set_attr(size_t smem) {
+    return cudaFuncSetAttribute(wpk::chain_lb_kernel<D, NOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int D>
+cudaError_t set_attr_d(int nop, size_t smem) {
+    return nop == 3 ? set_attr<D, 3>(smem) : set_attr<D, 2>(smem);
+}
+
+cudaError_t set_attr_any(int D, int nop, size_t smem) {
+    switch (D) {
+        case 2: return set_attr_d<2>(nop, smem);
+        case 4: return set_attr_d<4>(nop, smem);
+        case 6: return set_attr_d<6>(nop, smem);
+        case 8: return set_attr_d<8>(nop, smem);
+        case 10: return set_attr_d<10>(nop, smem);
+        case 12: return set_attr_d<12>(nop, smem);
+        case 14: return set_attr_d<14>(nop, smem);
+        case 16: return set_attr_d<16>(nop, smem);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+size_t lb_smem_bytes(int D, int H, int nop) {
+    return wpk::LbLayout(wpk::CT_TOUT + H, H + 64, D, nop).total;
+}
+
+bool lb_fits(int S, int T) {
+    if (S < 1 || S > 8) return false;
+    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
+    if (H > wpk::LB_MAX_H) return false;
+    return lb_smem_bytes(2 * S, H, 2) <= 227 * 1024;
+}
+
+void lb_free(LbPlan &p) {
+    if (p.d_bimg) cudaFree(p.d_bimg);
+    if (p.d_stabs) cudaFree(p.d_stabs);
+    if (p.d_MTl) cudaFree(p.d_MTl);
+    p.d_bimg = nullptr;
+    p.d_stabs = p.d_MTl = nullptr;
+}
+
+int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps_in, double gain,
+             std::string &err) {
+    const int D = 2 * S;
+    const std::vector<double> f = taps_in.empty() ? std::vector<double>{1.0} : taps_in;
+    const int T = (int)f.size();
+    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
+    const int K = H + 64, W = wpk::CT_TOUT + H;
+    if (!lb_fits(S, T)) {
+        err = "chain pass does not fit the single-pass kernel";
+        return WP_EUNSUP;
+    }
+    // ---- state space in the per-section balanced basis ----
+    MatL A0;
+    std::vector<LD> B0, C0;
+    LD d = 0;
+    cascade_df2t(sos, S, A0, B0, C0, d);
+    MatL Tm((size_t)D * D, 0.0L), Ti((size_t)D * D, 0.0L);
+    int balanced = 0;
+    for (int s = 0; s < S; ++s) {
+        LD t[4], ti[4];
+        if (!balance_section(&sos[5 * s], t, ti)) {
+            t[0] = t[3] = ti[0] = ti[3] = 1.0L;
+            t[1] = t[2] = ti[1] = ti[2] = 0.0L;
+        } else {
+            ++balanced;
+        }
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) {
+                Tm[(2 * s + i) * D + 2 * s + j] = t[i * 2 + j];
+                Ti[(2 * s + i) * D + 2 * s + j] = ti[i * 2 + j];
+            }
+    }
+    const MatL A = mat_mul(mat_mul(Tm, A0, D), Ti, D);
+    std::vector<LD> B(D, 0.0L), C(D, 0.0L);
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            B[i] += Tm[i * D + j] * B0[j];
+            C[j] += C0[i] * Ti[i * D + j];
+        }
+    // the transform keeps A block lower triangular; drop rounding residue above the blocks
+    MatL Ac = A;
+    for (int r = 0; r < D; ++r)
+        for (int q = wpk::lt_nj(r); q < D; ++q) Ac[r * D + q] = 0.0L;
+    // ---- C A^t, impulse response, combined response g, state term E, e weights ----
+    std::vector<LD> CA((size_t)(K + 1) * D);
+    {
+        std::vector<LD> row = C, nrow(D);
+        for (int t = 0; t <= K; ++t) {
+            for (int i = 0; i < D; ++i) CA[(size_t)t * D + i] = row[i];
+            for (int j = 0; j < D; ++j) {
+                LD acc = 0;
+                for (int i = 0; i < D; ++i) acc += row[i] * Ac[i * D + j];
+                nrow[j] = acc;
+            }
+            row = nrow;
+        }
+    }
+    std::vector<LD> h(K);
+    h[0] = d;
+    for (int t = 1; t < K; ++t) {
+        LD acc = 0;
+        for (int i = 0; i < D; ++i) acc += CA[(size_t)(t - 1) * D + i] * B[i];
+        h[t] = acc;
+    }
+    std::vector<double> g(K);
+    for (int t = 0; t < K; ++t) {
+        LD acc = 0;
+        for (int k = 0; k < T && k <= t; ++k) acc += (LD)f[k] * h[t - k];
+        g[t] = (double)(acc * (LD)gain);
+    }
+    std::vector<double> E((size_t)64 * D);
+    for (int q = 0; q < 64; ++q)
+        for (int i = 0; i < D; ++i) {
+            LD acc = 0;
+            for (int k = 0; k < T; ++k) acc += (LD)f[k] * CA[(size_t)(H + q - k) * D + i];
+            E[(size_t)q * D + i] = (double)(acc * (LD)gain);
+        }
+    std::vector<double> Ke((size_t)64 * D);
+    {
+        std::vector<LD> v = B, nv(D);
+        for (int n = 63; n >= 0; --n) {
+            for (int i = 0; i < D; ++i) Ke[(size_t)n * D + i] = (double)v[i];
+            for (int i = 0; i < D; ++i) {
+                LD acc = 0;
+                for (int j = 0; j < D; ++j) acc += Ac[i * D + j] * v[j];
+                nv[i] = acc;
+            }
+            v = nv;
+        }
+    }
+    // ---- B image: atom 0 [g_hi | g_lo | Ke_hi | Ke_lo], atoms >= 1 [g_hi | g_lo]; SW128 K-major ----
+    const int DE = wpk::lb_de(D), NS = wpk::lb_ns(D);
+    double gmax = 0;
+    for (double v : g) gmax = std::max(gmax, std::fabs(v));
+    const int fB = gmax > 0 ? 14 - exp_of(gmax) : 0;
+    p.out_scale = (float)std::ldexp(1.0, -fB);
+    int fK[16] = {0};
+    for (int i = 0; i < D; ++i) {
+        double km = 0;
+        for (int n = 0; n < 64; ++n) km = std::max(km, std::fabs(Ke[(size_t)n * D + i]));
+        fK[i] = km > 0 ? 14 - exp_of(km) : 0;
+        p.escale[i] = (float)std::ldexp(1.0, -fK[i]);
+    }
+    for (int i = D; i < 16; ++i) p.escale[i] = 0.f;
+    const int atoms = (K + 63) / 64;
+    const size_t b0Bytes = (size_t)NS * 128, bBytes = b0Bytes + (size_t)(atoms - 1) * 16384;
+    std::vector<__half> img(bBytes / 2, __float2half_rn(0.f));
+    auto put = [&](size_t base, int row, int kk, float val, bool lo) {
+        (void)lo;
+        const uint32_t logical = (uint32_t)row * 128u + (uint32_t)kk * 2u;
+        const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
+        img[(base + phys) / 2] = __float2half_rn(val);
+    };
+    for (int a = 0; a < atoms; ++a) {
+        const size_t base = a == 0 ? 0 : b0Bytes + (size_t)(a - 1) * 16384;
+        for (int kk = 0; kk < 64; ++kk) {
+            const int k = 64 * a + kk;
+            if (k >= K) break;
+            for (int q = 0; q < 64; ++q) {
+                const int t = q + H - k;
+                const float val = (t >= 0 && t < K) ? (float)std::ldexp(g[t], fB) : 0.f;
+                const __half hi = __float2half_rn(val);
+                put(base, q, kk, __half2float(hi), false);
+                put(base, 64 + q, kk, val - __half2float(hi), true);  // unscaled lo: one accumulator
+            }
+            if (a == 0) {
+                for (int i = 0; i < D; ++i) {
+                    const float val = (float)std::ldexp(Ke[(size_t)kk * D + i], fK[i]);
+                    const __half hi = __float2half_rn(val);
+                    put(base, 128 + i, kk, __half2float(hi), false);
+                    put(base, 128 + DE + i, kk, val - __half2float(hi), true);
+                }
+            }
+        }
+    }
+    // ---- scan tables ----
+    const MatL M = mat_pow(Ac, 64, D);
+    std::vector<float> st((size_t)wpk::lb_tab_floats(D), 0.f);
+    for (int q = 0; q < 64; ++q)
+        for (int i = 0; i < D; ++i) st[(size_t)q * D + i] = (float)E[(size_t)q * D + i];
+    {
+        MatL m = M;
+        for (int b = 0; b < 7; ++b) {
+            put_lt(&st[wpk::lb_off_mp(D) + b * wpk::lt_size(D)], m, D);
+            m = mat_mul(m, m, D);
+        }
+        const MatL M32 = mat_pow(M, 32, D);
+        MatL w = mat_eye(D);
+        for (int q = 0; q < 4; ++q) {
+            put_lt(&st[wpk::lb_off_wt(D) + q * wpk::lt_size(D)], w, D);
+            w = mat_mul(w, M32, D);
+        }
+        if (wpk::lb_has_gl(D)) {
+            MatL gm = mat_eye(D);
+            for (int l = 0; l < 32; ++l) {
+                for (int r = 0; r < D; ++r)
+                    for (int q = 0; q < wpk::lt_nj(r); ++q)
+                        st[wpk::lb_off_gl(D) + (size_t)(wpk::lt_off(r) + q) * 32 + l] = (float)gm[r * D + q];
+                gm = mat_mul(gm, M, D);
+            }
+        }
+    }
+    // look-back powers (M^128)^l, l < 32, lane-minor [D * D][32]; then M^128 dense
+    std::vector<float> mtl((size_t)D * D * 32 + (size_t)D * D);
+    {
+        const MatL MT = mat_pow(M, 128, D);
+        MatL m = mat_eye(D);
+        for (int l = 0; l < 32; ++l) {
+            for (int i = 0; i < D * D; ++i) mtl[(size_t)i * 32 + l] = (float)m[i];
+            m = mat_mul(m, MT, D);
+        }
+        for (int i = 0; i < D * D; ++i) mtl[(size_t)D * D * 32 + i] = (float)MT[i];
+    }
+    for (float v : st)
+        if (!std::isfinite(v)) {
+            err = "chain tables are not finite (unstable cascade?)";
+            return WP_EINVAL;
+        }
+    // ---- upload ----
+    cudaError_t e = cudaMalloc(&p.d_bimg, bBytes);
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_bimg, img.data(), bBytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_stabs, st.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_stabs, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_MTl, mtl.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_MTl, mtl.data(), mtl.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        err = std::string("chain table upload: ") + cudaGetErrorString(e);
+        return WP_ECUDA;
+    }
+    p.D = D;
+    p.H = H;
+    p.K = K;
+    p.W = W;
+    p.nop = lb_smem_bytes(D, H, 3) <= 227 * 1024 ? 3 : 2;
+    p.smem = lb_smem_bytes(D, H, p.nop);
+    // the attribute is per kernel, shared by every plan of this (D, stages) shape: set the maximum
+    e = set_attr_any(D, p.nop, 227 * 1024);
+    if (e != cudaSuccess) {
+        err = std::string("chain kernel attribute: ") + cudaGetErrorString(e);
+        return WP_ECUDA;
+    }
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "chain_lb[iir=%d fir=%d gain=%g] tcgen05 f16x3 M128xN%d K=%d halo=%d tile=%d stages=%d smem=%zu "
+             "fp32 scan (balanced basis, %d/%d sections), look-back",
+             S, T > 1 ? T : 0, gain, NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S);
+    p.desc = buf;
+    return WP_OK;
+}
+
+// published-state words: aggregates [tiles][D] + block-end states [blocks][C][D], 8 B each
+static size_t lb_words(const LbPlan &p, long long C, long long tiles) {
+    const long long T = tiles / C;
+    const long long blocks = (T + wpk::LB_BLK - 1) / wpk::LB_BLK;
+    return ((size_t)tiles + (size_t)blocks * C) * p.D;
+}
+
+size_t lb_workspace_bytes(const LbPlan &p, long long C, long long tiles) { return 8 * lb_words(p, C, tiles); }
+
+namespace {
+template <int D>
+cudaError_t launch_d(int nop, const wpk::LbArgs &a, int grid, size_t smem, cudaStream_t st) {
+    if (nop == 3)
+        wpk::chain_lb_kernel<D, 3><<<grid, wpk::LB_THREADS, smem, st>>>(a);
+    else
+        wpk::chain_lb_kernel<D, 2><<<grid, wpk::LB_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, long long N, long long ldx, long long ldy,
+                      void *ws, unsigned long long *trace, cudaStream_t st) {
+    const long long T = (N + wpk::CT_TOUT - 1) / wpk::CT_TOUT;
+    const long long tiles = T * C;
+    wpk::LbArgs a{};
+    a.x = x;
+    a.y = y;
+    a.C = C;
+    a.N = N;
+    a.ldx = ldx;
+    a.ldy = ldy;
+    a.total_tiles = tiles;
+    a.H = p.H;
+    a.K = p.K;
+    a.W = p.W;
+    a.Bimg = p.d_bimg;
+    a.stabs = p.d_stabs;
+    a.MTl = p.d_MTl;
+    a.out_scale = p.out_scale;
+    for (int i = 0; i < 16; ++i) a.escale[i] = p.escale[i];
+    a.aggw = reinterpret_cast<unsigned long long *>(ws);
+    a.inclw = a.aggw + (size_t)tiles * p.D;
+    a.vec_x = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+    a.vec_y = (ldy % 4 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    a.trace = trace;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * lb_words(p, C, tiles), st);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)std::min<long long>(tiles, sm_count());
+    switch (p.D) {
+        case 2: e = launch_d<2>(p.nop, a, grid, p.smem, st); break;
+        case 4: e = launch_d<4>(p.nop, a, grid, p.smem, st); break;
+        case 6: e = launch_d<6>(p.nop, a, grid, p.smem, st); break;
+        case 8: e = launch_d<8>(p.nop, a, grid, p.smem, st); break;
+        case 10: e = launch_d<10>(p.nop, a, grid, p.smem, st); break;
+        case 12: e = launch_d<12>(p.nop, a, grid, p.smem, st); break;
+        case 14: e = launch_d<14>(p.nop, a, grid, p.smem, st); break;
+        case 16: e = launch_d<16>(p.nop, a, grid, p.smem, st); break;
+        default: return cudaErrorInvalidValue;
+    }
+    count_launch();
+    return e;
+}
+
+}  // namespace wp

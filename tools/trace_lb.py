@@ -1,0 +1,62 @@
+"""Per-tile role timeline of chain_lb (diagnostics): python tools/trace_lb.py [cfg3|cfg5] [seconds]
+Events (ns, %globaltimer): 0 converter start, 1 operands ready, 2 MMA start, 3 MMAs issued,
+4 look-back start, 5 look-back done, 6 scan done (aggregate published), 7 epilogue done,
+8 epilogue start, 9 TMEM read (accumulator free), 10 carry received, 11 state term done."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import bench  # noqa: E402
+import paper_2504_08624_b200 as wp  # noqa: E402
+from paper_2504_08624_b200 import _native, engine  # noqa: E402
+
+EV = 12
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+cfg = bench.CONFIGS[name]
+C, fs = cfg["C"], cfg["fs"]
+dur = float(sys.argv[2]) if len(sys.argv) > 2 else (cfg["dur"] if name != "cfg5" else 20.0)
+N = int(round(dur * fs))
+stages = wp.Chain(bench.stages_for(name, wp)).bind(fs).stages
+x = wp.white_noise(dur, C, fs, seed=42).tensor()
+y = torch.empty_like(x)
+plan = engine.plan_for(stages, device=0)
+print(plan.describe_for(C, N))
+nb = plan.workspace_bytes(C, N)
+ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+st = torch.cuda.current_stream().cuda_stream
+tiles = C * ((N + 8191) // 8192)
+tr = torch.zeros(tiles * EV, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
+e1.record()
+torch.cuda.synchronize()
+print("ms per pass (untraced): %.4f" % (e0.elapsed_time(e1) / 10))
+_native.set_trace(tr.data_ptr(), tr.numel())
+plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
+torch.cuda.synchronize()
+_native.set_trace(0, 0)
+t = tr.cpu().numpy().astype(np.float64).reshape(tiles, EV)
+t0 = t[t > 0].min()
+t = np.where(t > 0, t - t0, np.nan)
+names = ["conv0", "opfull", "mma0", "mma1", "lb0", "lbdone", "scan1", "epi1", "-", "carry", "s", "-"]
+print("span us: %.1f" % (np.nanmax(t[:, 7]) / 1e3))
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 6), (4, 5), (6, 9), (5, 9), (9, 10), (10, 7), (0, 7)]:
+    d = (t[:, b] - t[:, a]) / 1e3
+    print(f"{names[a]:>6} -> {names[b]:<6} median {np.nanmedian(d):7.2f} us  p90 {np.nanpercentile(d, 90):7.2f}")
+G = min(tiles, 148)
+for ev in range(EV):
+    per = []
+    for b in range(G):
+        col = t[b::G, ev]
+        col = col[~np.isnan(col)]
+        if col.size > 2:
+            per.append(np.median(np.diff(col)))
+    print(f"per-CTA period of {names[ev]:>6}: median {np.median(per) / 1e3:.2f} us")
