@@ -115,6 +115,16 @@ __device__ __forceinline__ uint64_t desc32(uint32_t saddr) {
     return d;
 }
 
+// no-swizzle K-major: LBO = 128 B (next core matrix along K), SBO = sbo (next 8-row group)
+__device__ __forceinline__ uint64_t desc_sbo(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(128u >> 4) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1u << 46;
+    return d;
+}
+
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }

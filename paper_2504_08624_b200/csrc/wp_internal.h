@@ -109,6 +109,8 @@ struct LbPlan {
     size_t smem = 0;
     unsigned char *d_bimg = nullptr;
     float *d_stabs = nullptr, *d_MTl = nullptr;
+    unsigned char *d_bsimg = nullptr;  // state-term B operand
+    float st_mul = 1.f;
     float out_scale = 1.f;
     float escale[16] = {};
     std::string desc;

@@ -157,6 +157,27 @@ bool balance_section(const double *sec, LD T[4], LD Ti[4]) {
     return true;
 }
 
+// W = A W A^T + Q (D x D, Smith doubling: W = sum_k A^k Q A^kT)
+MatL lyap_doubling(const MatL &A, const MatL &Q, int D) {
+    MatL W = Q, Ak = A;
+    for (int it = 0; it < 64; ++it) {
+        // W += Ak W Ak^T
+        MatL AkT((size_t)D * D);
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) AkT[i * D + j] = Ak[j * D + i];
+        const MatL add = mat_mul(mat_mul(Ak, W, D), AkT, D);
+        LD delta = 0, norm = 0;
+        for (int i = 0; i < D * D; ++i) {
+            W[i] += add[i];
+            delta = std::max(delta, std::fabs(add[i]));
+            norm = std::max(norm, std::fabs(W[i]));
+        }
+        Ak = mat_mul(Ak, Ak, D);
+        if (delta <= 1e-19L * norm) break;
+    }
+    return W;
+}
+
 // DF2T cascade state space (states w1, w2 per section, section-major)
 void cascade_df2t(const std::vector<double> &sos, int S, MatL &A, std::vector<LD> &B, std::vector<LD> &C, LD &d) {
     const int D = 2 * S;
@@ -184,9 +205,10 @@ void cascade_df2t(const std::vector<double> &sos, int S, MatL &A, std::vector<LD
     d = step(e, 1.0L, B);
 }
 
-void put_lt(float *dst, const MatL &m, int D) {
+void put_dense(float *dst, const MatL &m, int D) {
+    const int DP = wpk::lb_dp(D);
     for (int r = 0; r < D; ++r)
-        for (int q = 0; q < wpk::lt_nj(r); ++q) dst[wpk::lt_off(r) + q] = (float)m[r * D + q];
+        for (int q = 0; q < DP; ++q) dst[r * DP + q] = (q < D && q < wpk::lt_nj(r)) ? (float)m[r * D + q] : 0.f;
 }
 
 int exp_of(double v) {
@@ -236,6 +258,8 @@ void lb_free(LbPlan &p) {
     if (p.d_bimg) cudaFree(p.d_bimg);
     if (p.d_stabs) cudaFree(p.d_stabs);
     if (p.d_MTl) cudaFree(p.d_MTl);
+    if (p.d_bsimg) cudaFree(p.d_bsimg);
+    p.d_bsimg = nullptr;
     p.d_bimg = nullptr;
     p.d_stabs = p.d_MTl = nullptr;
 }
@@ -272,13 +296,38 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
                 Ti[(2 * s + i) * D + 2 * s + j] = ti[i * 2 + j];
             }
     }
-    const MatL A = mat_mul(mat_mul(Tm, A0, D), Ti, D);
+    MatL A = mat_mul(mat_mul(Tm, A0, D), Ti, D);
     std::vector<LD> B(D, 0.0L), C(D, 0.0L);
     for (int i = 0; i < D; ++i)
         for (int j = 0; j < D; ++j) {
             B[i] += Tm[i * D + j] * B0[j];
             C[j] += C0[i] * Ti[i * D + j];
         }
+    {
+        // diagonal re-balancing against the WHOLE cascade's Gramians: a section's
+        // own balancing does not see the gain of the sections around it (e.g. the
+        // cascade gain folded into section 0), which can leave E ~ 1e4 x the
+        // states; s_i -> alpha_i s_i with alpha_i = (Wo_ii / Wc_ii)^(1/4) keeps the
+        // block structure and brings |E| |s| back to the output's scale
+        MatL Qc((size_t)D * D), Qo((size_t)D * D), At((size_t)D * D);
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) {
+                Qc[i * D + j] = B[i] * B[j];
+                Qo[i * D + j] = C[i] * C[j];
+                At[i * D + j] = A[j * D + i];
+            }
+        const MatL Wc = lyap_doubling(A, Qc, D), Wo = lyap_doubling(At, Qo, D);
+        std::vector<LD> al(D, 1.0L);
+        for (int i = 0; i < D; ++i) {
+            const LD c = Wc[i * D + i], o = Wo[i * D + i];
+            if (c > 0 && o > 0 && std::isfinite((double)c) && std::isfinite((double)o)) al[i] = std::pow(o / c, 0.25L);
+        }
+        for (int i = 0; i < D; ++i) {
+            B[i] *= al[i];
+            C[i] /= al[i];
+            for (int j = 0; j < D; ++j) A[i * D + j] *= al[i] / al[j];
+        }
+    }
     // the transform keeps A block lower triangular; drop rounding residue above the blocks
     MatL Ac = A;
     for (int r = 0; r < D; ++r)
@@ -330,11 +379,13 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
             v = nv;
         }
     }
-    // ---- B image: atom 0 [g_hi | g_lo | Ke_hi | Ke_lo], atoms >= 1 [g_hi | g_lo]; SW128 K-major ----
-    const int DE = wpk::lb_de(D), NS = wpk::lb_ns(D);
+    // ---- B images per K atom: hi then lo, SW128 K-major; atom 0 rows [g (64) | Ke (D) | 0], others [g] ----
+    const int DE = wpk::lb_de(D);
     double gmax = 0;
     for (double v : g) gmax = std::max(gmax, std::fabs(v));
-    const int fB = gmax > 0 ? 14 - exp_of(gmax) : 0;
+    // g is scaled to < 2^8 (not 2^14): the accumulator scale (tile scale x 2^fB) then leaves the
+    // fp16 state operand s x tile scale x 2^(fB - fE) ~ 2^10 of headroom before it overflows
+    const int fB = gmax > 0 ? 7 - exp_of(gmax) : 0;
     p.out_scale = (float)std::ldexp(1.0, -fB);
     int fK[16] = {0};
     for (int i = 0; i < D; ++i) {
@@ -345,16 +396,15 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     }
     for (int i = D; i < 16; ++i) p.escale[i] = 0.f;
     const int atoms = (K + 63) / 64;
-    const size_t b0Bytes = (size_t)NS * 128, bBytes = b0Bytes + (size_t)(atoms - 1) * 16384;
+    const size_t bBytes = wpk::lb_bbytes(K);
     std::vector<__half> img(bBytes / 2, __float2half_rn(0.f));
-    auto put = [&](size_t base, int row, int kk, float val, bool lo) {
-        (void)lo;
+    auto put = [&](size_t base, int row, int kk, float val) {
         const uint32_t logical = (uint32_t)row * 128u + (uint32_t)kk * 2u;
         const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
         img[(base + phys) / 2] = __float2half_rn(val);
     };
     for (int a = 0; a < atoms; ++a) {
-        const size_t base = a == 0 ? 0 : b0Bytes + (size_t)(a - 1) * 16384;
+        const size_t bh = wpk::lb_bhi(a), bl = wpk::lb_blo(a);
         for (int kk = 0; kk < 64; ++kk) {
             const int k = 64 * a + kk;
             if (k >= K) break;
@@ -362,15 +412,15 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
                 const int t = q + H - k;
                 const float val = (t >= 0 && t < K) ? (float)std::ldexp(g[t], fB) : 0.f;
                 const __half hi = __float2half_rn(val);
-                put(base, q, kk, __half2float(hi), false);
-                put(base, 64 + q, kk, val - __half2float(hi), true);  // unscaled lo: one accumulator
+                put(bh, q, kk, __half2float(hi));
+                put(bl, q, kk, val - __half2float(hi));  // lo part, same scale: one accumulator
             }
             if (a == 0) {
                 for (int i = 0; i < D; ++i) {
                     const float val = (float)std::ldexp(Ke[(size_t)kk * D + i], fK[i]);
                     const __half hi = __float2half_rn(val);
-                    put(base, 128 + i, kk, __half2float(hi), false);
-                    put(base, 128 + DE + i, kk, val - __half2float(hi), true);
+                    put(bh, 64 + i, kk, __half2float(hi));
+                    put(bl, 64 + i, kk, val - __half2float(hi));
                 }
             }
         }
@@ -383,13 +433,13 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     {
         MatL m = M;
         for (int b = 0; b < 7; ++b) {
-            put_lt(&st[wpk::lb_off_mp(D) + b * wpk::lt_size(D)], m, D);
+            put_dense(&st[wpk::lb_off_mp(D) + b * D * wpk::lb_dp(D)], m, D);
             m = mat_mul(m, m, D);
         }
         const MatL M32 = mat_pow(M, 32, D);
         MatL w = mat_eye(D);
         for (int q = 0; q < 4; ++q) {
-            put_lt(&st[wpk::lb_off_wt(D) + q * wpk::lt_size(D)], w, D);
+            put_dense(&st[wpk::lb_off_wt(D) + q * D * wpk::lb_dp(D)], w, D);
             w = mat_mul(w, M32, D);
         }
         if (wpk::lb_has_gl(D)) {
@@ -413,6 +463,21 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
         }
         for (int i = 0; i < D * D; ++i) mtl[(size_t)D * D * 32 + i] = (float)MT[i];
     }
+    // state-term B operand [64 rows][KS] fp16: row p = [E_hi | E_hi | E_lo | 0] (x [s_hi | s_lo | s_hi])
+    double emax = 0;
+    for (double v : E) emax = std::max(emax, std::fabs(v));
+    const int fE = emax > 0 ? 14 - exp_of(emax) : 0;
+    p.st_mul = (float)std::ldexp(1.0, fB - fE);
+    const int KS = wpk::lb_ks(D);
+    std::vector<__half> bs((size_t)64 * KS, __float2half_rn(0.f));
+    for (int q = 0; q < 64; ++q)
+        for (int k = 0; k < KS; ++k) {
+            const int part = k / DE, d = k % DE;
+            if (d >= D || part > 2) continue;
+            const float val = (float)std::ldexp(E[(size_t)q * D + d], fE);
+            const __half hi = __float2half_rn(val);
+            bs[wpk::lb_s_off(D, q, k) / 2] = part < 2 ? hi : __float2half_rn(val - __half2float(hi));
+        }
     for (float v : st)
         if (!std::isfinite(v)) {
             err = "chain tables are not finite (unstable cascade?)";
@@ -423,6 +488,8 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     if (e == cudaSuccess) e = cudaMemcpy(p.d_bimg, img.data(), bBytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p.d_stabs, st.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p.d_stabs, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_bsimg, bs.size() * sizeof(__half));
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_bsimg, bs.data(), bs.size() * sizeof(__half), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p.d_MTl, mtl.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p.d_MTl, mtl.data(), mtl.size() * sizeof(float), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -445,7 +512,7 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     snprintf(buf, sizeof buf,
              "chain_lb[iir=%d fir=%d gain=%g] tcgen05 f16x3 M128xN%d K=%d halo=%d tile=%d stages=%d smem=%zu "
              "fp32 scan (balanced basis, %d/%d sections), look-back",
-             S, T > 1 ? T : 0, gain, NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S);
+             S, T > 1 ? T : 0, gain, wpk::LB_NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S);
     p.desc = buf;
     return WP_OK;
 }
@@ -488,6 +555,8 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     a.Bimg = p.d_bimg;
     a.stabs = p.d_stabs;
     a.MTl = p.d_MTl;
+    a.Bsimg = p.d_bsimg;
+    a.st_mul = p.st_mul;
     a.out_scale = p.out_scale;
     for (int i = 0; i < 16; ++i) a.escale[i] = p.escale[i];
     a.aggw = reinterpret_cast<unsigned long long *>(ws);

@@ -92,6 +92,18 @@ __device__ __forceinline__ bool mbar_try(uint32_t saddr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// non-blocking probe of an mbarrier phase
+__device__ __forceinline__ bool mbar_test(uint32_t saddr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 done, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, done;\n\t}\n"
+        : "=r"(ok)
+        : "r"(saddr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ unsigned long long now_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -101,6 +113,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t saddr, uint32_t parity) {
     if (mbar_try(saddr, parity)) return;
     const unsigned long long t0 = now_ns();
     while (!mbar_try(saddr, parity)) {
+        if (now_ns() - t0 > 10000000000ull) asm volatile("trap;");
+    }
+}
+// The same with an exponential nanosleep back-off (capped at MAXNS) between
+// polls: the suspend hint above returns early whenever any barrier of the CTA
+// changes, so a warp that is far ahead would otherwise spin and take issue
+// slots from the warps it is waiting for.
+template <unsigned MAXNS>
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t saddr, uint32_t parity) {
+    if (mbar_try(saddr, parity)) return;
+    const unsigned long long t0 = now_ns();
+    unsigned ns = 32;
+    while (!mbar_try(saddr, parity)) {
+        __nanosleep(ns);
+        ns = ns < MAXNS ? 2 * ns : MAXNS;
         if (now_ns() - t0 > 10000000000ull) asm volatile("trap;");
     }
 }

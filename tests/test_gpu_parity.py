@@ -283,11 +283,11 @@ def test_cfg3_full_size_prefix_parity():
 def test_plan_launch_accounting():
     plan = _native.Plan(tuple(wp.engine._entry(s) for s in wp.Chain(_cfg3()).bind(48000).stages))
     assert plan.num_passes == 1  # IIR(4 sections) -> FIR -> gain fused into one pass
-    # one pass = chain_rows + chain_carry + chain_gemm (no intermediate signal in HBM)
-    assert plan.launches == 3
+    # one pass = one chain_lb launch (no intermediate signal in HBM)
+    assert plan.launches == 1
     before = _native.launch_count()
     wp.pipe(wp.white_noise(1.0, 2, 48000, seed=1), wp.Chain(_cfg3())).tensor()
-    assert _native.launch_count() - before == 4  # noise + the pass's three kernels
+    assert _native.launch_count() - before == 2  # noise + the pass's kernel
 
 
 @pytest.mark.parametrize("scale", [1e-6, 1.0, 3e4, 1e9])
@@ -324,8 +324,9 @@ def test_fir_tensor_core_zeros_and_tail():
     "stages, fs, shape, kernel",
     [
         (lambda: [wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
-                  wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, (32, 5760000), "chain_gemm"),  # cfg3
-        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1024, 14400000), "chain_gemm"),      # cfg5
+                  wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, (32, 5760000), "chain_lb"),  # cfg3
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1024, 14400000), "chain_lb"),      # cfg5
+        (lambda: _bench_chain(), 44100, (2, 88200), "chain_lb"),                                    # 8 SOS: one pass
         (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (4, 48000), "fused"),                 # small IIR
         (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, (2, 441000), "fused"),                # cfg1
         (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, (8, 2880000), "fir_tc"),          # cfg2
@@ -338,7 +339,7 @@ def test_plan_uses_intended_kernel(stages, fs, shape, kernel):
     plan = engine.plan_for(wp.Chain(stages()).bind(fs).stages, device=0)
     desc = plan.describe_for(*shape)
     assert len(desc) == 1 and kernel in desc[0].split("[")[0], desc
-    assert plan.launches_for(*shape) == (3 if kernel == "chain_gemm" else 1)
+    assert plan.launches_for(*shape) == 1
 
 
 # ---- host -> device -> host streaming (pinned sources, channel blocks) -------
@@ -428,7 +429,7 @@ def test_many_channels_lp8_subset_parity():
         assert oracle.parity_error(y[c:c + 1], ref) <= IIR_TOL, c
 
 
-# ---- the three-kernel chain (chain_rows -> chain_carry -> chain_gemm) ---------
+# ---- chain passes: single-pass chain_lb (default) and the round-1 three-kernel chain (WP_CHAIN_IMPL=tc)
 
 
 @pytest.mark.gpu
@@ -499,7 +500,7 @@ def test_chain_pass_stopband_input_f64():
 @pytest.mark.gpu
 def test_multi_pass_chain_normalize_chain():
     """chain pass -> Normalize -> chain pass: ping-pong buffers, workspace reuse
-    and the dependent launches of consecutive three-kernel passes."""
+    and workspace reuse between consecutive single-pass chains."""
     fs = 48000
     stages = [wp.design_butterworth("hp", 4, 120, fs), wp.design_fir("lp", 33, 9000, fs=fs), wp.Normalize(0.8),
               wp.design_chebyshev1("lp", 4, 1.0, 6000, fs), wp.design_fir("lp", 65, 12000, fs=fs), wp.Gain(0.5)]
@@ -509,7 +510,7 @@ def test_multi_pass_chain_normalize_chain():
 
     plan = engine.plan_for(wp.Chain(stages).bind(fs).stages, device=0)
     desc = plan.describe_for(3, 50001)
-    assert len(desc) == 3 and "chain_gemm" in desc[0] and desc[1].startswith("normalize") and "chain_gemm" in desc[2]
+    assert len(desc) == 3 and "chain_lb" in desc[0] and desc[1].startswith("normalize") and "chain_lb" in desc[2]
     y = wp.pipe(w, wp.Chain(stages)).samples
     ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
     assert oracle.parity_error(y, ref) <= IIR_TOL
@@ -517,8 +518,8 @@ def test_multi_pass_chain_normalize_chain():
 
 @pytest.mark.gpu
 def test_plan_execute_in_cuda_graph():
-    """plan.execute never allocates or synchronises, so a chain pass (three
-    kernels with dependent launches) can be captured once and replayed."""
+    """plan.execute never allocates or synchronises, so a chain pass (record
+    memset + chain_lb) can be captured once and replayed."""
     import torch
 
     from paper_2504_08624_b200 import engine
