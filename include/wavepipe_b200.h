@@ -96,18 +96,26 @@ int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames);
 const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t channels, int64_t frames);
 
 /* ---- seam-level one-shot entry points (mirror _kernels_jit functions) ----
- * Each builds a transient plan, executes it, and frees it after the stream
- * has passed the call (the free is stream-ordered via cudaLaunchHostFunc). */
+ * Each looks up (or builds) a plan for its single stage in a small
+ * process-wide cache (64 entries, LRU; shared ownership, so a plan evicted
+ * while another thread executes it stays alive until that call returns) and
+ * executes it. The *_workspace queries return the workspace bytes one call of
+ * that shape needs (it grows with channels x frames for IIR passes: published
+ * tile states, ~1 B per 128 samples per state). */
 
 /* iir_cascade_{serial,parallel}(sos, x) (_kernels_jit.py:35-48) */
 int wp_iir_cascade(const double *sos, int32_t n_sections, const float *x, float *y, int64_t channels,
                    int64_t frames, int64_t ld_x, int64_t ld_y, int32_t flags, void *workspace,
                    size_t workspace_bytes, wp_stream_t stream);
+int wp_iir_cascade_workspace(const double *sos, int32_t n_sections, int64_t channels, int64_t frames, int32_t flags,
+                             size_t *bytes);
 /* fir_direct_{serial,parallel}(taps, x) (_kernels_jit.py:65-78) and
  * engine._fir_fft (engine.py:206-223) selected by flags */
 int wp_fir(const double *taps, int32_t n_taps, const float *x, float *y, int64_t channels, int64_t frames,
            int64_t ld_x, int64_t ld_y, int32_t flags, void *workspace, size_t workspace_bytes,
            wp_stream_t stream);
+int wp_fir_workspace(const double *taps, int32_t n_taps, int64_t channels, int64_t frames, int32_t flags,
+                     size_t *bytes);
 
 /* ---- signal sources and reductions ---- */
 

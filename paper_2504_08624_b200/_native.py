@@ -46,6 +46,8 @@ EXPORTED = (
     "wp_plan_describe_for",
     "wp_iir_cascade",
     "wp_fir",
+    "wp_iir_cascade_workspace",
+    "wp_fir_workspace",
     "wp_white_noise",
     "wp_peak_abs",
     "wp_last_error",
@@ -101,6 +103,8 @@ def load(require_device: bool = False):
             lib.wp_plan_describe_for.restype = ctypes.c_char_p
             lib.wp_iir_cascade.argtypes = [dp, i32, vp, vp, i64, i64, i64, i64, i32, vp, sz, vp]
             lib.wp_fir.argtypes = [dp, i32, vp, vp, i64, i64, i64, i64, i32, vp, sz, vp]
+            lib.wp_iir_cascade_workspace.argtypes = [dp, i32, i64, i64, i32, ctypes.POINTER(sz)]
+            lib.wp_fir_workspace.argtypes = [dp, i32, i64, i64, i32, ctypes.POINTER(sz)]
             lib.wp_white_noise.argtypes = [vp, i64, i64, i64, ctypes.c_uint64, vp]
             lib.wp_peak_abs.argtypes = [vp, i64, i64, i64, vp, vp]
             lib.wp_last_error.restype = ctypes.c_char_p
@@ -110,6 +114,7 @@ def load(require_device: bool = False):
             lib.wp_wav_encode.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp]
             for name in ("wp_plan_create", "wp_plan_destroy", "wp_plan_workspace_bytes", "wp_plan_execute",
                          "wp_plan_num_passes", "wp_plan_launches", "wp_plan_launches_for", "wp_iir_cascade", "wp_fir",
+                         "wp_iir_cascade_workspace", "wp_fir_workspace",
                          "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace",
                          "wp_wav_decode", "wp_wav_encode"):
                 getattr(lib, name).restype = ctypes.c_int

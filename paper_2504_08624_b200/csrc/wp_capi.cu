@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -38,8 +39,6 @@ thread_local std::string g_err;
 unsigned long long *g_trace = nullptr;  // diagnostics: per-tile stage timestamps (wp_set_trace)
 size_t g_trace_entries = 0;
 std::atomic<unsigned long long> g_launches{0};
-std::atomic<unsigned long long> g_epoch{0};
-std::once_flag g_epoch_once;
 
 int fail(int code, const std::string &msg) {
     g_err = msg;
@@ -49,19 +48,6 @@ int fail(int code, const std::string &msg) {
 int cuda_fail(cudaError_t e, const char *what) {
     g_err = std::string(what) + ": " + cudaGetErrorString(e);
     return WP_ECUDA;
-}
-
-unsigned long long next_epoch() {
-    std::call_once(g_epoch_once, [] {
-        // random 62-bit start so stale look-back flags left in recycled device
-        // memory can never carry the current epoch
-        unsigned long long t = (unsigned long long)std::chrono::high_resolution_clock::now().time_since_epoch().count();
-        t ^= (unsigned long long)getpid() * 0x9E3779B97F4A7C15ull;
-        t ^= t >> 29;
-        t *= 0xBF58476D1CE4E5B9ull;
-        g_epoch.store((t & ((1ull << 61) - 1)) | 1ull);
-    });
-    return g_epoch.fetch_add(1) & ((1ull << 62) - 1);
 }
 
 constexpr double kF64Radius = 0.98;
@@ -1233,7 +1219,9 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.G = p.d_G;
             a.TP = p.d_TP;
             a.recs = ws + rec_off;
-            a.epoch = next_epoch();
+            a.epoch = 1;
+            e = cudaMemsetAsync(a.recs, 0, rec_bytes(p) * (size_t)(((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C), stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset(records)");
             a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
             a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
             {
@@ -1290,9 +1278,13 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.TP = p.d_TP;
             a.counter = counter;
             a.recs = ws + rec_off;
-            a.epoch = next_epoch();
             const long long tpc = tiles_per_channel(p, N);
             a.total_tiles = tpc * C;
+            // look-back records are zeroed by every launch (stream-ordered, so a
+            // captured CUDA graph replays correctly); flags then carry epoch 1
+            a.epoch = 1;
+            e = cudaMemsetAsync(a.recs, 0, rec_bytes(p) * (size_t)a.total_tiles, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset(records)");
             const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
             e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
             if (e != cudaSuccess) return cuda_fail(e, "memset(counter)");
@@ -1307,30 +1299,58 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
 }
 
 // ---- seam-level one-shot entry points with a small plan cache ----
+// Plans are shared (std::shared_ptr): a caller holds its reference for the
+// duration of the execute call, so evicting an entry never frees a plan that
+// another thread is still using (the last holder destroys it; cudaFree
+// synchronizes the device, so in-flight launches complete first).
 static std::mutex g_cache_mu;
-static std::map<std::string, wp_plan *> g_cache;
+static std::map<std::string, std::pair<std::shared_ptr<wp_plan>, unsigned long long>> g_cache;
+static unsigned long long g_cache_clock = 0;
 
-static int cached_plan(const wp_stage &st, wp_plan **out) {
+static int cached_plan(const wp_stage &st, std::shared_ptr<wp_plan> *out) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::string key((const char *)&st.kind, sizeof st.kind);
     key.append((const char *)&st.flags, sizeof st.flags);
     key.append((const char *)&dev, sizeof dev);
     key.append((const char *)st.coef, sizeof(double) * (size_t)st.n * (st.kind == WP_STAGE_IIR ? 5 : 1));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_cache.find(key);
+        if (it != g_cache.end()) {
+            it->second.second = ++g_cache_clock;
+            *out = it->second.first;
+            return WP_OK;
+        }
+    }
+    wp_plan *raw = nullptr;
+    const int rc = wp_plan_create(&st, 1, &raw);
+    if (rc != WP_OK) return rc;
+    std::shared_ptr<wp_plan> sp(raw, [](wp_plan *p) { wp_plan_destroy(p); });
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
-    if (it != g_cache.end()) {
-        *out = it->second;
+    if (it != g_cache.end()) {  // another thread built the same plan meanwhile
+        *out = it->second.first;
         return WP_OK;
     }
     if (g_cache.size() >= 64) {
-        // rare path: drop everything (cudaFree synchronizes the device)
-        for (auto &kv : g_cache) wp_plan_destroy(kv.second);
-        g_cache.clear();
+        // evict the least recently used entry (holders keep it alive)
+        auto lru = g_cache.begin();
+        for (auto jt = g_cache.begin(); jt != g_cache.end(); ++jt)
+            if (jt->second.second < lru->second.second) lru = jt;
+        g_cache.erase(lru);
     }
-    int rc = wp_plan_create(&st, 1, out);
-    if (rc == WP_OK) g_cache[key] = *out;
-    return rc;
+    g_cache[key] = {sp, ++g_cache_clock};
+    *out = sp;
+    return WP_OK;
+}
+
+static int seam_workspace(const wp_stage &st, int64_t channels, int64_t frames, size_t *bytes) {
+    if (!bytes) return fail(WP_EINVAL, "bytes is NULL");
+    std::shared_ptr<wp_plan> plan;
+    const int rc = cached_plan(st, &plan);
+    if (rc != WP_OK) return rc;
+    return wp_plan_workspace_bytes(plan.get(), channels, frames, bytes);
 }
 
 int wp_iir_cascade(const double *sos, int32_t n_sections, const float *x, float *y, int64_t channels, int64_t frames,
@@ -1338,20 +1358,32 @@ int wp_iir_cascade(const double *sos, int32_t n_sections, const float *x, float 
                    wp_stream_t stream) {
     wp_stage st{WP_STAGE_IIR, n_sections, sos, 0.0, flags, 0};
     if (n_sections < 1 || !sos) return fail(WP_EINVAL, "need >= 1 section");
-    wp_plan *plan = nullptr;
+    std::shared_ptr<wp_plan> plan;
     int rc = cached_plan(st, &plan);
     if (rc != WP_OK) return rc;
-    return wp_plan_execute(plan, x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+    return wp_plan_execute(plan.get(), x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+}
+
+int wp_iir_cascade_workspace(const double *sos, int32_t n_sections, int64_t channels, int64_t frames, int32_t flags,
+                             size_t *bytes) {
+    if (n_sections < 1 || !sos) return fail(WP_EINVAL, "need >= 1 section");
+    return seam_workspace(wp_stage{WP_STAGE_IIR, n_sections, sos, 0.0, flags, 0}, channels, frames, bytes);
 }
 
 int wp_fir(const double *taps, int32_t n_taps, const float *x, float *y, int64_t channels, int64_t frames, int64_t ld_x,
            int64_t ld_y, int32_t flags, void *workspace, size_t workspace_bytes, wp_stream_t stream) {
     wp_stage st{WP_STAGE_FIR, n_taps, taps, 0.0, flags, 0};
     if (n_taps < 1 || !taps) return fail(WP_EINVAL, "need >= 1 tap");
-    wp_plan *plan = nullptr;
+    std::shared_ptr<wp_plan> plan;
     int rc = cached_plan(st, &plan);
     if (rc != WP_OK) return rc;
-    return wp_plan_execute(plan, x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+    return wp_plan_execute(plan.get(), x, y, channels, frames, ld_x, ld_y, workspace, workspace_bytes, stream);
+}
+
+int wp_fir_workspace(const double *taps, int32_t n_taps, int64_t channels, int64_t frames, int32_t flags,
+                     size_t *bytes) {
+    if (n_taps < 1 || !taps) return fail(WP_EINVAL, "need >= 1 tap");
+    return seam_workspace(wp_stage{WP_STAGE_FIR, n_taps, taps, 0.0, flags, 0}, channels, frames, bytes);
 }
 
 int wp_white_noise(float *y, int64_t channels, int64_t frames, int64_t ld_y, uint64_t seed, wp_stream_t stream) {
