@@ -15,7 +15,15 @@ reference's generator (seed 42). Input + output (737 MB + 737 MB) exceed the
 
 Multi-GPU (torchrun, one process per GPU): every rank filters its own
 32-channel batch (weak scaling, no collective on the data path); the step
-time is the max over ranks of the CUDA-event time.
+time is the max over ranks of the CUDA-event time. The same run also measures
+the north star's strong-scaling case, cfg5's fixed 1024 channels split over
+the ranks by ``sharding.partition`` (``strong_cfg5`` in the JSON line; at N=1
+it is the single-GPU reference point of that curve). ``--config cfgX
+--scaling strong`` makes any config the headline in strong-scaling form.
+
+Every line checks the timed output against the CPU oracle: the first and the
+last 0.5 s of the first and last channel (for IIR chains the oracle runs the
+whole channels, so the tail check covers the cross-tile state carry).
 
 --impl reference: the reference's CPU algorithm (oracle/ port of the numba
 kernels, bit-identical to them) on the host cores, on a bounded time slice of
@@ -156,6 +164,39 @@ def _cpu_describe(name, x, dur_s, threads, times):
             f"reference numba kernels (float64, bit-identical), {threads} threads over channels")
 
 
+def parity_check(name, wp, x_dev, y_dev, fs):
+    """Head and tail of the first and last channel of the timed output vs the
+    oracle port (the only oracle use on this arm; after the timed region)."""
+    import numpy as np
+
+    import oracle
+
+    stages = wp.Chain(stages_for(name, wp)).bind(fs).stages
+    C, N = x_dev.shape
+    n = min(N, fs // 2)
+    chans = sorted({0, C - 1})
+    fir_only = all(hasattr(st, "taps") for st in stages if not hasattr(st, "factor"))
+    taps = sum(len(st.taps) - 1 for st in stages if hasattr(st, "taps"))
+    out = {}
+    for c in chans:
+        if fir_only:
+            # causal FIR: the tail depends only on the last n + T - 1 samples
+            lo = max(0, N - n - taps)
+            xs = x_dev[c:c + 1, lo:].double().cpu().numpy()
+            ref_tail = oracle.pipe(xs, stages)[:, -n:]
+            ref_head = oracle.pipe(x_dev[c:c + 1, :n].double().cpu().numpy(), stages)
+        else:
+            ref = oracle.pipe(x_dev[c:c + 1].double().cpu().numpy(), stages, oracle.default_threads())
+            ref_head, ref_tail = ref[:, :n], ref[:, -n:]
+        y = y_dev[c:c + 1]
+        out[f"ch{c}_head"] = oracle.parity_error(y[:, :n].double().cpu().numpy(), ref_head)
+        out[f"ch{c}_tail"] = oracle.parity_error(y[:, -n:].double().cpu().numpy(), ref_tail)
+    worst = max(out.values())
+    return {"max_abs_err_over_peak": worst, "bar": 1e-5 if fir_only else 1e-4, "windows": out,
+            "sample": f"first and last {n} frames of channels {chans} of the timed output vs the oracle port "
+                      f"({'windowed FIR' if fir_only else 'whole channels'})"}
+
+
 def cpu_baseline(name, wp, budget_s=8.0):
     """Reference CPU algorithm on the box's host cores (bench._run_cell
     protocol: 1 untimed warm-up, perf_counter around the apply only)."""
@@ -221,6 +262,10 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every rank filters the whole config; strong: the config's channels are split")
+    ap.add_argument("--no-strong-cfg5", action="store_true", help="skip the cfg5 strong-scaling side measurement")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed output")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -246,84 +291,124 @@ def main():
 
     name = args.config
     cfg = CONFIGS[name]
-    C, fs = cfg["C"], cfg["fs"]
+    C_cfg, fs = cfg["C"], cfg["fs"]
     N = int(round(cfg["dur"] * fs))
     stages = wp.Chain(stages_for(name, wp)).bind(fs).stages
     dev = torch.device("cuda", local_rank)
+    from paper_2504_08624_b200.sharding import partition
 
-    # ---- inputs resident in HBM (device noise, distinct seed per rank) ----
-    w = wp.white_noise(cfg["dur"], C, fs, seed=42 + rank, device=dev)
-    x = w.tensor()
-    y = torch.empty_like(x)
-    plan = engine.plan_for(stages, device=local_rank)
-    stream = torch.cuda.current_stream(dev)
-    nbytes = plan.workspace_bytes(C, N)
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    if args.scaling == "strong":
+        c0, c1 = partition(C_cfg, world)[rank]
+        C = c1 - c0
+    else:
+        C = C_cfg
 
-    def step():
-        plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nbytes, stream.cuda_stream)
+    def max_over_ranks(vals):
+        if not dist:
+            return vals
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        # keep the GPU busy ~0.5 s before warm-up so the clock samples (every
-        # 100 ms) see the part under this load, then W warm-up steps, then K
-        settle = time.perf_counter()
-        while time.perf_counter() - settle < 0.5:
-            step()
+    def timed(plan, x, y, Cr, Nr, steps, warmup, clk_gpu=None):
+        """CUDA-event time of `steps` plan executions after `warmup` (barrier +
+        synchronize on both sides); returns (ms_per_step, per_launch_ms, launches, clocks)."""
+        stream = torch.cuda.current_stream(dev)
+        nbytes = plan.workspace_bytes(max(Cr, 1), Nr)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+        def step():
+            if Cr > 0:
+                plan.execute(x.data_ptr(), y.data_ptr(), Cr, Nr, Nr, Nr, ws.data_ptr(), nbytes, stream.cuda_stream)
+
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local_rank) if clk_gpu else None
+        if sampler:
+            sampler.__enter__()
+        try:
+            # keep the GPU busy ~0.5 s before warm-up so the clock samples (every
+            # 100 ms) see the part under this load, then W warm-up steps, then K
+            settle = time.perf_counter()
+            while time.perf_counter() - settle < 0.5:
+                step()
+                torch.cuda.synchronize()
+            for _ in range(warmup):
+                step()
             torch.cuda.synchronize()
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            launches0 = _native.launch_count()
+            t_start.record(stream)
+            for i in range(steps):
+                ev[i][0].record(stream)
+                step()
+                ev[i][1].record(stream)
+            t_end.record(stream)
+            torch.cuda.synchronize()
+            launches = _native.launch_count() - launches0
+        finally:
+            if sampler:
+                sampler.__exit__(None, None, None)
+        elapsed_ms = t_start.elapsed_time(t_end)
+        per_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        elapsed_ms, per_launch_ms = max_over_ranks([elapsed_ms, per_launch_ms])
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        launches0 = _native.launch_count()
-        t_start.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    launches = _native.launch_count() - launches0
-    elapsed_ms = t_start.elapsed_time(t_end)
-    per_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    if dist:
-        t = torch.tensor([elapsed_ms, per_launch_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, per_launch_ms = t.tolist()
-        dist.barrier()
+        return elapsed_ms / steps, per_launch_ms, launches, (sampler.summary() if sampler else None)
 
-    ms_per_step = elapsed_ms / args.steps
+    # ---- headline: inputs resident in HBM (device noise, distinct seed per rank) ----
+    w = wp.white_noise(cfg["dur"], max(C, 1), fs, seed=42 + rank, device=dev)
+    x = w.tensor()[:C]
+    y = torch.empty_like(x)
+    plan = engine.plan_for(stages, device=local_rank)
+    ms_per_step, per_launch_ms, launches, clocks = timed(plan, x, y, C, N, args.steps, args.warmup, clk_gpu=True)
     units = C * N
-    value = units * world / (ms_per_step / 1e3)
+    total_units = units * world if args.scaling == "weak" else C_cfg * N
+    value = total_units / (ms_per_step / 1e3)
 
-    # part of the CPU-baseline leg (the only place this arm touches oracle/):
-    # the timed output's first 0.5 s of channel 0 against the port
-    parity = None
-    n_chk = min(N, fs // 2)
-    with_baseline = not args.no_cpu_baseline and world == 1
-    if with_baseline:
-        import oracle
-
-        ref = oracle.pipe(x[:1, :n_chk].double().cpu().numpy(), stages)
-        parity = oracle.parity_error(y[:1, :n_chk].double().cpu().numpy(), ref)
+    # the timed output against the oracle (rank 0, after the timed region)
+    with_baseline = not args.no_cpu_baseline and rank == 0 and world == 1
+    parity = parity_check(name, wp, x, y, fs) if rank == 0 and C > 0 and not args.no_parity else None
     host_in = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
     host_in.copy_(x)
-    # free the device-resident bench buffers before the end-to-end leg (cfg5
-    # is 59 GB per buffer: in + out + e2e in + e2e out would not fit)
-    del x, y, ws, w
+    # free the device-resident bench buffers before the other legs (cfg5 is
+    # 59 GB per buffer: in + out + e2e in + e2e out would not fit)
+    del x, y, w
     torch.cuda.empty_cache()
+
+    # ---- north-star strong scaling: cfg5's 1024 channels split over the ranks ----
+    strong = None
+    if not args.no_strong_cfg5 and not (name == "cfg5" and args.scaling == "strong"):
+        c5 = CONFIGS["cfg5"]
+        N5 = int(round(c5["dur"] * c5["fs"]))
+        a0, a1 = partition(c5["C"], world)[rank]
+        C5 = a1 - a0
+        w5 = wp.white_noise(c5["dur"], max(C5, 1), c5["fs"], seed=1042 + rank, device=dev)
+        x5 = w5.tensor()[:C5]
+        y5 = torch.empty_like(x5)
+        plan5 = engine.plan_for(wp.Chain(stages_for("cfg5", wp)).bind(c5["fs"]).stages, device=local_rank)
+        ms5, pl5, _, _ = timed(plan5, x5, y5, C5, N5, min(args.steps, 10), 3)
+        strong = {"workload": c5["workload"], "config_id": "cfg5", "scaling": "strong", "n_gpus": world,
+                  "channels_total": c5["C"], "channels_per_gpu_max": max(b - a for a, b in partition(c5["C"], world)),
+                  "frames": N5, "ms_per_step": ms5, "value": c5["C"] * N5 / (ms5 / 1e3), "unit": "ch-samples/s",
+                  "per_gpu_hbm_frac": 8.0 * max(b - a for a, b in partition(c5["C"], world)) * N5 / (pl5 / 1e3) / 1e9
+                  / load_peaks()[0],
+                  "partition": "sharding.partition (contiguous, pair-aligned channel blocks), no collectives",
+                  "passes": plan5.describe_for(max(C5, 1), N5)}
+        del x5, y5, w5
+        torch.cuda.empty_cache()
 
     # ---- end to end through the public API: pinned host in -> host out ----
     host_out = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
     chain = wp.Chain(stages_for(name, wp))
 
     def e2e_step():
-        src = wp.Wave.from_tensor(host_in, fs)
-        (src | chain).numpy32(out=host_out)
+        if C > 0:
+            src = wp.Wave.from_tensor(host_in, fs)
+            (src | chain).numpy32(out=host_out)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -335,11 +420,7 @@ def main():
         e2e_step()
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
-    e2e_s = statistics.mean(e2e_times)
-    if dist:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = t.item()
+    e2e_s = max_over_ranks([statistics.mean(e2e_times)])[0]
 
     if rank != 0:
         if dist:
@@ -348,8 +429,8 @@ def main():
 
     hbm_peak, bf16_peak, peak_kind = load_peaks()
     algo_bytes = 8.0 * units  # fp32 read once + write once per channel-sample
-    passes = plan.describe_for(C, N)
-    kernel_names = {"chain_tc": "wpk::chain_tc_kernel", "fir_tc": "wpk::fir_tc_kernel",
+    passes = plan.describe_for(max(C, 1), N)
+    kernel_names = {"chain_lb": "wpk::chain_lb_kernel", "fir_tc": "wpk::fir_tc_kernel",
                     "chain_rows+chain_carry+chain_gemm":
                         "wpk::chain_rows_kernel + wpk::chain_carry_kernel + wpk::chain_gemm_kernel",
                     "fft_ols": "wpk::fft_ols_kernel", "fused": "wpk::fused_chain_kernel"}
@@ -364,7 +445,7 @@ def main():
             traffic = ent["dram_bytes_per_unit"] * units if "dram_bytes_per_unit" in ent else ent.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    clocks = clk.summary()
+    io_mb = units * 4 / 1e6
     line = {
         "metric": "channel-samples/s for FIR & IIR chains at 1/8 B200; % of HBM roofline",
         "value": value,
@@ -374,25 +455,31 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
-        "dtype": "f32 I/O; IIR scan f64 for pole radius > 0.98 (cfg3 HP), else f32",
+        "dtype": "f32 I/O and f32 scan/state (balanced state basis); tensor-core f16x3 split products",
         "data": "synthetic white noise generated on device (reference generator, seed 42+rank)",
         "config": {"workload": cfg["workload"], "config_id": name, "channels_per_gpu": C, "frames": N, "fs": fs,
-                   "l2": "inputs larger than L2 (737 MB in + 737 MB out per step), no flush",
-                   "passes": passes, "parallelism": f"channel batches x{world}, no collectives"},
+                   "l2": f"inputs larger than L2 ({io_mb:.0f} MB in + {io_mb:.0f} MB out per step), no flush"
+                   if io_mb > 126 else f"{io_mb:.0f} MB in + out per step: partly L2-resident between steps",
+                   "passes": passes,
+                   "parallelism": f"channel batches x{world} ({args.scaling} scaling), no collectives"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": per_launch_ms,
-                     "kernel": " + ".join(kernels) + f" ({plan.launches_for(C, N)} launch(es) per step)"},
-        "e2e": {"value": units * world / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
+                     "kernel": " + ".join(kernels) + f" ({plan.launches_for(max(C, 1), N)} launch(es) per step)"},
+        "e2e": {"value": total_units / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,
                 "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned)"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if strong is not None:
+        line["strong_cfg5"] = strong
+    if parity is not None:
+        line["parity_check"] = parity
     taps = sum(len(getattr(st, "taps", ())) for st in stages)
-    if any(("chain_tc" in k or "fir_tc" in k or "chain_gemm" in k) for k in kernels) and taps:
+    if any(("chain_lb" in k or "fir_tc" in k or "chain_gemm" in k) for k in kernels) and taps:
         # algorithmic FIR flops = 2 T per channel-sample, against
         # the dense fp16 tensor peak; the fp16 x3 split runs 3x those MMAs
         tflops = 2.0 * taps * units / (per_launch_ms / 1e3) / 1e12
@@ -401,8 +488,7 @@ def main():
                                       "note": "algorithmic 2*T flops/ch-sample; executed MMA work is 3x (fp16 hi/lo split)"}
     if with_baseline:
         line["cpu_baseline"] = cpu_baseline(name, wp)
-        line["cpu_baseline"]["parity_check"] = {"max_abs_err_over_peak": parity,
-                                                "sample": f"ch0 first {n_chk} frames of the timed output vs this port"}
+        line["cpu_baseline"]["parity_check"] = parity  # the same check, kept here for round-1 readers
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

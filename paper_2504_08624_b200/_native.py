@@ -231,6 +231,20 @@ class Plan:
         )
 
 
+def peak_abs(tensor) -> float:
+    """max |x| of a float32 CUDA tensor [C, N] (device reduction, one float back)."""
+    import torch
+
+    lib = load(require_device=True)
+    t = tensor.contiguous()
+    C, N = t.shape
+    out = torch.empty(1, dtype=torch.float32, device=t.device)
+    with torch.cuda.device(t.device):
+        check(lib.wp_peak_abs(t.data_ptr(), C, N, N, out.data_ptr(), torch.cuda.current_stream(t.device).cuda_stream),
+              "wp_peak_abs")
+    return float(out.item())
+
+
 def white_noise(y_ptr: int, channels: int, frames: int, ld: int, seed: int, stream: int) -> None:
     lib = load(require_device=True)
     check(lib.wp_white_noise(y_ptr, channels, frames, ld, seed & 0xFFFFFFFFFFFFFFFF, stream), "wp_white_noise")

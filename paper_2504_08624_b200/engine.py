@@ -266,6 +266,21 @@ def _copy_streams(device):
     return _streams[key]
 
 
+def has_normalize(entries) -> bool:
+    """A Normalize stage needs the peak of the WHOLE wave (design.Normalize), so
+    such a chain cannot run block by block."""
+    return any(k == _native.WP_STAGE_NORMALIZE for (k, _c, _v, _f) in entries)
+
+
+def normalize_scale(peak: float, target: float):
+    """The factor scale_by_peak applies (fp32 target / fp32 peak), None for an
+    all-zero input (returned unchanged)."""
+    p = np.float32(peak)
+    if not p > 0:
+        return None
+    return float(np.float32(target) / p)
+
+
 def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 0):
     """Host -> device -> host execution of a recorded chain, overlapped.
 
@@ -282,6 +297,8 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     from .sharding import partition
 
     _require_cuda()
+    if has_normalize(entries):
+        raise InvalidArgument("a chain with Normalize needs the whole wave's peak: it cannot be streamed in blocks")
     C, N = host_src.shape
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):

@@ -107,7 +107,8 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
             continue
         with torch.cuda.device(dev):
             part = (src[c0:c1] if src is not None else host_src[c0:c1]).to(dev, non_blocking=True)
-            shards.append(((c0, c1), dev, (Wave._wrap_device(part.contiguous(), wave.fs) | chain)))
+            shards.append(((c0, c1), dev, Wave._wrap_device(part.contiguous(), wave.fs)))
+    shards = _run_segments(shards, chain, lambda peaks: max(peaks))
     if gather is None:
         return [w for _, _, w in shards]
     out = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
@@ -117,6 +118,52 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
     for _, dev, _ in shards:
         torch.cuda.synchronize(dev)
     return Wave.from_tensor(out, wave.fs)
+
+
+def _run_segments(shards, chain, combine_peaks):
+    """Apply a bound chain to every shard. Stages between Normalize stages run
+    as one lazy (fused) chain per shard; a Normalize takes the peak over ALL
+    shards (``combine_peaks``: host max, or an all-reduce across ranks) and
+    applies the same fp32 factor as the unsharded scale_by_peak, as its own
+    pass, so results stay bit-identical to the single-device run."""
+    from .chain import Chain
+    from .design import Gain, Normalize
+    from .engine import normalize_scale
+    from ._native import peak_abs
+
+    torch = _torch()
+    seg = []
+    stages = list(chain.stages) + [None]
+    for st in stages:
+        if st is not None and not isinstance(st, Normalize):
+            seg.append(st)
+            continue
+        if seg:
+            fs = shards[0][2].fs if shards else None
+            new = []
+            for blk, dev, w in shards:
+                with torch.cuda.device(dev):
+                    y = w | Chain(seg).bind(fs)
+                    y.tensor()  # materialise: the next step is a separate pass
+                new.append((blk, dev, y))
+            shards = new
+            seg = []
+        if st is None:
+            break
+        peaks = []
+        for _, dev, w in shards:
+            with torch.cuda.device(dev):
+                peaks.append(peak_abs(w.tensor()))
+        factor = normalize_scale(combine_peaks(peaks) if peaks else 0.0, st.peak)
+        if factor is not None:
+            new = []
+            for blk, dev, w in shards:
+                with torch.cuda.device(dev):
+                    y = w | Gain(factor)
+                    y.tensor()
+                new.append((blk, dev, y))
+            shards = new
+    return shards
 
 
 def gather_blocks(local, channels: int, group=None, dst: int = 0):
@@ -155,7 +202,18 @@ def distributed_pipe(local: Wave, stages, channels: int, group=None, gather_to: 
     Wave as a second element)."""
     import torch.distributed as dist
 
-    out = local | _chain(stages)
+    import torch
+
+    chain = _chain(stages).bind(local.fs)
+
+    def allreduce_max(peaks):
+        t = torch.tensor([max(peaks) if peaks else 0.0], dtype=torch.float32,
+                         device=local.tensor().device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return float(t.item())
+
+    dev = local.tensor().device
+    out = _run_segments([((0, local.channels), dev, local)], chain, allreduce_max)[0][2]
     if gather_to is None:
         return out, None
     full = gather_blocks(out.tensor(), channels, group=group, dst=gather_to)

@@ -198,8 +198,12 @@ class Wave:
         """A pending chain over a host-resident (pinned) source: its result can
         be streamed host -> device -> host in channel blocks."""
         src = self._src
-        return (self._entries is not None and src is not None and src._dev is None and src._entries is None
-                and src._pinned is not None)
+        if not (self._entries is not None and src is not None and src._dev is None and src._entries is None
+                and src._pinned is not None):
+            return False
+        from .engine import has_normalize
+
+        return not has_normalize(self._entries)  # Normalize needs the whole wave's peak
 
     def numpy32(self, out=None) -> np.ndarray:
         """Float32 host copy (``out`` may be a preallocated, e.g. pinned, array

@@ -550,3 +550,40 @@ def test_plan_execute_in_cuda_graph():
     assert torch.equal(y_graph, y_eager)
     ref = oracle.pipe(x.double().cpu().numpy(), bound)
     assert oracle.parity_error(y_graph.double().cpu().numpy(), ref) <= IIR_TOL
+
+
+# ---- LTI fuser coverage: whole runs of IIR / FIR / gain stages in one pass ----
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["bench_chain_8sos", "fir_then_iir", "iir_fir241_gain", "two_firs_iir",
+                                  "iir_long_fir_split"])
+def test_fuser_passes_and_parity(name):
+    """The reference's pinned 8-SOS chain (bench.py:93-100) and its mixed FIR ->
+    IIR chain (test_chain.py:167-173) run as ONE pass; a FIR too long for the
+    single-pass kernel gets its own FIR-only pass after the IIR pass."""
+    fs = 44100 if name in ("bench_chain_8sos", "fir_then_iir") else 48000
+    chains = {
+        "bench_chain_8sos": (_bench_chain(), 1),
+        "fir_then_iir": ([wp.design_fir("lowpass", 33, 4000), wp.design_peaking(1000, gain_db=2.0)], 1),
+        "iir_fir241_gain": ([wp.design_chebyshev1("lp", 4, 1.0, 5000), wp.design_fir("lp", 241, 9000), wp.Gain(0.7)], 1),
+        "two_firs_iir": ([wp.design_fir("lp", 61, 9000), wp.design_butterworth("hp", 2, 80),
+                          wp.design_fir("lp", 41, 12000)], 1),
+        "iir_long_fir_split": ([wp.design_butterworth("hp", 4, 100), wp.design_fir("lp", 8193, 3000)], 2),
+    }
+    stages, passes = chains[name]
+    bound = wp.Chain(stages).bind(fs).stages
+    from paper_2504_08624_b200 import engine
+
+    plan = engine.plan_for(bound, device=0)
+    assert plan.num_passes == passes, plan.describe()
+    rng = np.random.default_rng(len(name))
+    w = wp.Wave(rng.standard_normal((3, 70001)), fs)
+    y = wp.pipe(w, wp.Chain(stages)).samples
+    ref = oracle.pipe(w.samples, bound)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
+    # pipe == stage-by-stage application (the reference's chain/step coherence)
+    step = w
+    for st in bound:
+        step = st.apply(step)
+    assert np.array_equal(step.samples, y)

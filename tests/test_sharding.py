@@ -108,3 +108,42 @@ def test_shard_pipe_fft_path_pairs_bit_exact():
     assert np.array_equal(got, ref)
     shards = wp.shard_pipe(w, fir, devices=[0, 0], gather=None)
     assert [s.channels for s in shards] == [4, 2]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C", [3, 8])
+def test_shard_pipe_normalize_uses_the_global_peak(C):
+    """Normalize over a sharded wave takes the peak of ALL channels (not each
+    shard's own), bit-identical to the unsharded chain (high)."""
+    fs = 48000
+    rng = np.random.default_rng(C)
+    x = rng.standard_normal((C, 30000))
+    x[-1] *= 10.0  # the loudest channel lives on the last shard only
+    w = wp.Wave(x, fs)
+    chain = wp.Chain([wp.design_butterworth("hp", 4, 100), wp.Normalize(0.8),
+                      wp.design_fir("lp", 33, 9000), wp.Gain(0.5)])
+    ref = (w | chain).samples
+    for devices in ([0, 0], [0, 0, 0]):
+        got = wp.shard_pipe(w, chain, devices=devices).samples
+        assert np.array_equal(got, ref), devices
+    assert np.max(np.abs(ref[:, :]))  # sanity
+
+
+@pytest.mark.gpu
+def test_pinned_source_chain_with_normalize_is_not_streamed_per_block():
+    """A lazy chain with Normalize over a pinned host source is materialised on
+    the whole wave (one peak), not streamed block by block (high)."""
+    import torch
+
+    fs = 48000
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((6, 40000)).astype(np.float32)
+    x[0] *= 5.0
+    chain = wp.Chain([wp.design_butterworth("lp", 4, 2000), wp.Normalize(1.0)])
+    ref = (wp.Wave(x.astype(np.float64), fs) | chain).samples
+    pinned = torch.from_numpy(x).pin_memory()
+    lazy = wp.Wave.from_tensor(pinned, fs) | chain
+    assert not lazy._host_streamable()
+    got = lazy.numpy32().astype(np.float64)
+    assert np.array_equal(got, ref)
+    assert np.max(np.abs(got)) == pytest.approx(1.0, rel=1e-6)
