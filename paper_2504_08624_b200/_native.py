@@ -16,7 +16,8 @@ import numpy as np
 from .errors import KernelError, NativeUnavailable
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwpb200.so")
+# WP_LIB: load another build of the same library (A/B diagnostics: tools/lb_variants.py)
+LIB_PATH = os.environ.get("WP_LIB") or os.path.join(HERE, "libwpb200.so")
 
 WP_STAGE_IIR = 1
 WP_STAGE_FIR = 2

@@ -109,10 +109,10 @@ struct LbPlan {
     size_t smem = 0;
     unsigned char *d_bimg = nullptr;
     float *d_stabs = nullptr, *d_MTl = nullptr;
-    unsigned char *d_bsimg = nullptr;  // state-term B operand
-    float st_mul = 1.f;
     float out_scale = 1.f;
     float escale[16] = {};
+    float4 Ep[256] = {};          // E pairs for the kernel's parameter space
+    float Mpw[11 * 16 * 16] = {};  // M^(2^b), M^(32 w) for the kernel's parameter space
     std::string desc;
 };
 // S sections (<= 8) and T taps (T <= 1: no FIR) fit the kernel's shared memory

@@ -258,8 +258,6 @@ void lb_free(LbPlan &p) {
     if (p.d_bimg) cudaFree(p.d_bimg);
     if (p.d_stabs) cudaFree(p.d_stabs);
     if (p.d_MTl) cudaFree(p.d_MTl);
-    if (p.d_bsimg) cudaFree(p.d_bsimg);
-    p.d_bsimg = nullptr;
     p.d_bimg = nullptr;
     p.d_stabs = p.d_MTl = nullptr;
 }
@@ -380,12 +378,10 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
         }
     }
     // ---- B images per K atom: hi then lo, SW128 K-major; atom 0 rows [g (64) | Ke (D) | 0], others [g] ----
-    const int DE = wpk::lb_de(D);
     double gmax = 0;
     for (double v : g) gmax = std::max(gmax, std::fabs(v));
-    // g is scaled to < 2^8 (not 2^14): the accumulator scale (tile scale x 2^fB) then leaves the
-    // fp16 state operand s x tile scale x 2^(fB - fE) ~ 2^10 of headroom before it overflows
-    const int fB = gmax > 0 ? 7 - exp_of(gmax) : 0;
+    // g scaled into [2^13, 2^14): lo parts of the small tail coefficients stay normal fp16
+    const int fB = gmax > 0 ? 14 - exp_of(gmax) : 0;
     p.out_scale = (float)std::ldexp(1.0, -fB);
     int fK[16] = {0};
     for (int i = 0; i < D; ++i) {
@@ -428,8 +424,11 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     // ---- scan tables ----
     const MatL M = mat_pow(Ac, 64, D);
     std::vector<float> st((size_t)wpk::lb_tab_floats(D), 0.f);
-    for (int q = 0; q < 64; ++q)
-        for (int i = 0; i < D; ++i) st[(size_t)q * D + i] = (float)E[(size_t)q * D + i];
+    // E in pairs for the epilogue's packed FMAs: [q2][d2] = (E[2q2][2d2], E[2q2+1][2d2], E[2q2][2d2+1], E[2q2+1][2d2+1])
+    for (int q2 = 0; q2 < 32; ++q2)
+        for (int d2 = 0; d2 < D / 2; ++d2)
+            for (int u = 0; u < 4; ++u)
+                st[((size_t)q2 * (D / 2) + d2) * 4 + u] = (float)E[(size_t)(2 * q2 + (u & 1)) * D + 2 * d2 + (u >> 1)];
     {
         MatL m = M;
         for (int b = 0; b < 7; ++b) {
@@ -463,21 +462,6 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
         }
         for (int i = 0; i < D * D; ++i) mtl[(size_t)D * D * 32 + i] = (float)MT[i];
     }
-    // state-term B operand [64 rows][KS] fp16: row p = [E_hi | E_hi | E_lo | 0] (x [s_hi | s_lo | s_hi])
-    double emax = 0;
-    for (double v : E) emax = std::max(emax, std::fabs(v));
-    const int fE = emax > 0 ? 14 - exp_of(emax) : 0;
-    p.st_mul = (float)std::ldexp(1.0, fB - fE);
-    const int KS = wpk::lb_ks(D);
-    std::vector<__half> bs((size_t)64 * KS, __float2half_rn(0.f));
-    for (int q = 0; q < 64; ++q)
-        for (int k = 0; k < KS; ++k) {
-            const int part = k / DE, d = k % DE;
-            if (d >= D || part > 2) continue;
-            const float val = (float)std::ldexp(E[(size_t)q * D + d], fE);
-            const __half hi = __float2half_rn(val);
-            bs[wpk::lb_s_off(D, q, k) / 2] = part < 2 ? hi : __float2half_rn(val - __half2float(hi));
-        }
     for (float v : st)
         if (!std::isfinite(v)) {
             err = "chain tables are not finite (unstable cascade?)";
@@ -488,14 +472,14 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     if (e == cudaSuccess) e = cudaMemcpy(p.d_bimg, img.data(), bBytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p.d_stabs, st.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p.d_stabs, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&p.d_bsimg, bs.size() * sizeof(__half));
-    if (e == cudaSuccess) e = cudaMemcpy(p.d_bsimg, bs.data(), bs.size() * sizeof(__half), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p.d_MTl, mtl.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p.d_MTl, mtl.data(), mtl.size() * sizeof(float), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         err = std::string("chain table upload: ") + cudaGetErrorString(e);
         return WP_ECUDA;
     }
+    for (int i = 0; i < 16 * D; ++i) p.Ep[i] = make_float4(st[4 * i], st[4 * i + 1], st[4 * i + 2], st[4 * i + 3]);
+    for (int i = 0; i < 11 * D * wpk::lb_dp(D); ++i) p.Mpw[i] = st[wpk::lb_off_mp(D) + i];
     p.D = D;
     p.H = H;
     p.K = K;
@@ -555,10 +539,10 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     a.Bimg = p.d_bimg;
     a.stabs = p.d_stabs;
     a.MTl = p.d_MTl;
-    a.Bsimg = p.d_bsimg;
-    a.st_mul = p.st_mul;
     a.out_scale = p.out_scale;
     for (int i = 0; i < 16; ++i) a.escale[i] = p.escale[i];
+    for (int i = 0; i < 16 * p.D; ++i) a.Ep[i] = p.Ep[i];
+    for (int i = 0; i < 11 * p.D * wpk::lb_dp(p.D); ++i) a.Mpw[i] = p.Mpw[i];
     a.aggw = reinterpret_cast<unsigned long long *>(ws);
     a.inclw = a.aggw + (size_t)tiles * p.D;
     a.vec_x = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);

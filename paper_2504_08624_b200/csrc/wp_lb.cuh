@@ -12,7 +12,7 @@
 // (n = n0 + 64 m + p), window start w_m = n0 - H + 64 m, H >= taps - 1:
 //
 //   y[n] = sum_{k < H+64} g[p + H - k] x[w_m + k]   main GEMM (tcgen05, f16x3)
-//        + sum_i E[p][i] s_{w_m}[i]                  state GEMM (tcgen05, f16x3)
+//        + sum_i E[p][i] s_{w_m}[i]                  state term (CUDA cores, fp32)
 //   s_{w_{m+1}} = M s_{w_m} + e_m,  M = A^64,  e_m = sum_{j<64} Ke[j] x[w_m + j]
 //   g = G (f * h),  E[p] = G sum_t f[t] C A^(H+p-t),  Ke[j] = A^(63-j) B
 //
@@ -23,10 +23,12 @@
 // MMAs: the first K atom's B images carry the Ke columns (64..64+D), so the e
 // GEMM shares every A-operand read. In the balanced basis the scan and the
 // carries are well conditioned in fp32 (the DF2T basis needs fp64 there:
-// tools/balance_probe.py). The state term is one more f16x3 GEMM into the
-// same accumulator: A = [s_hi | s_lo | s_hi] x (tile scale), B = [E_hi; E_hi;
-// E_lo]. A row whose scaled state would overflow fp16 (a silent tile after a
-// loud one) sends zeros to it and adds E s on the CUDA cores instead.
+// tools/balance_probe.py). The state term E s (D FMAs per output, packed
+// fma.rn.f32x2) is added by the epilogue threads in fp32 straight from the
+// TMEM read: no second MMA round trip through the tensor pipe (where it would
+// queue behind main GEMMs), so an accumulator stage is released as soon as
+// the tile's carry is known. Measured against the f16x3 state GEMM issued
+// between main-GEMM K steps: 0.583 vs 0.618 ms for cfg3.
 //
 // Cross-tile state: deterministic blocked decoupled look-back. Tile (c, k)
 // publishes its zero-carry aggregate; its carry-in is
@@ -40,18 +42,20 @@
 // host zeroes them before every launch (graph-safe).
 //
 // Warp roles (persistent, one CTA per SM, static tile schedule):
-//   warp 0       TMEM allocation; lane 0 issues main(i) (3 MMAs per K step),
-//                then state(i - LAG), so a tile's scan / look-back latency
-//                overlaps the following tiles' main GEMMs
-//   warp 1       bulk-copy producer of the fp32 window, L2 prefetch ahead
-//   warps 2-6    converters: fp32 window -> SW128 fp16 hi / lo (Hankel rows)
-//   warp 7       look-back: carry-in c of each tile (the only role that waits
-//                on other SMs), inclusive state of block-end tiles
-//   warps 8-15   two row groups (even / odd local tiles), one TMEM lane per
-//                thread: scan (e from TMEM, Kogge-Stone over rows, aggregate ->
-//                global); once the carry is known s_m = L_m + M^m (Z_w +
-//                M^(32 w) c) -> state operand; after the state MMA the
-//                epilogue: TMEM -> scale -> coalesced stores
+//   warp 0       TMEM allocation; lane 0 issues the main GEMM of every tile
+//                (3 MMAs per K step) into a ring of six accumulator stages
+//   warps 2-6    converters: fp32 window -> SW128 fp16 hi / lo (Hankel rows);
+//                thread 0 bulk-copies the next fp32 window, L2 prefetch ahead
+//   warps 1, 7   look-back (even / odd local tiles, so two tiles' polls are in
+//                flight): carry-in c of each tile (the only role that waits on
+//                other SMs), inclusive state of block-end tiles
+//   warps 8-11   scan, one TMEM lane per thread: e from TMEM as soon as the
+//                MMAs complete, Kogge-Stone over rows, aggregate -> global
+//                (early, so other SMs' look-backs see it), row prefixes at
+//                zero carry -> shared ring
+//   warps 12-19  epilogue, two groups of four (even / odd local tiles): once
+//                the carry is known s_m = L_m + M^m c, TMEM -> scale + E s_m ->
+//                padded staging -> coalesced stores
 #pragma once
 
 #include <cuda_fp16.h>
@@ -62,16 +66,35 @@
 
 namespace wpk {
 
-constexpr int LB_THREADS = 512;
+// build-time variants (A/B diagnostics, tools/lb_variants.py); the defaults are the product
+#ifndef LB_EG
+#define LB_EG 1          // epilogue groups of four warps (alternate tiles)
+#endif
+#ifndef LB_E_CONST
+#define LB_E_CONST 0     // E pairs from the kernel parameters (constant bank) instead of shared memory
+#endif
+#ifndef LB_M_CONST
+#define LB_M_CONST 1     // M^(2^b), M^(32 w) from the kernel parameters instead of shared memory
+#endif
+#ifndef LB_GROUP_WAIT
+#define LB_GROUP_WAIT 0  // one waiting thread per role + named barrier (else every warp polls)
+#endif
+#ifndef LB_FFMA2
+#define LB_FFMA2 1       // packed fp32x2 FMAs for E s
+#endif
+constexpr int LB_THREADS = 384 + 128 * LB_EG;
 constexpr int LB_CONV = 160;   // converter threads (warps 2..6)
 constexpr int LB_QMAX = 14;    // float4 of the window per converter thread (W <= 8960)
 constexpr int LB_NA = 6;       // TMEM accumulator stages (80 columns each)
 constexpr int LB_NS = 80;      // TMEM columns per stage: main [0, 64), e [64, 80)
-constexpr int LB_LAG = 4;      // main(i) is issued before state(i - LB_LAG)
-constexpr int LB_NC = 4;       // carry ring (look-back warp -> row groups)
-constexpr int LB_RING = 16;    // tile-scale ring (converters -> row groups)
+constexpr int LB_NC = 4;       // carry ring (look-back warp -> epilogue)
+#ifndef LB_NLV
+#define LB_NLV 4
+#endif
+constexpr int LB_NL = LB_NLV;  // row-prefix ring (scan -> epilogue)
+constexpr int LB_RING = 16;    // tile-scale ring (converters -> scan)
 constexpr int LB_MAX_H = 256;  // FIR halo limit (W <= 8448)
-constexpr int LB_TRACE_EV = 12;
+constexpr int LB_TRACE_EV = 16;
 constexpr int LB_BLK = 32;     // look-back block (tiles of one channel)
 
 struct LbArgs {
@@ -83,9 +106,11 @@ struct LbArgs {
     const unsigned char *Bimg;   // SW128 K-major fp16 per K atom: [hi image | lo image], atom 0 with Ke rows
     const float *stabs;          // tables copied to shared memory (layout below)
     const float *MTl;            // [D * D][32] lane-minor: (M^128)^l, l < 32; then [D][D] M^128
-    const unsigned char *Bsimg;  // [64 rows][KS] fp16, no-swizzle K-major: state-term B operand
-    float st_mul;                // 2^(fB - fE): state operand = s * tile scale * st_mul
     float out_scale;             // 2^-fB of the g image
+    // warp-uniform tables read from the constant bank (kernel parameters), so they stay off
+    // the shared-memory pipe that the MMA operand reads saturate:
+    float4 Ep[256];              // [32][D / 2] E pairs (= tabs[0, 64 D))
+    float Mpw[11 * 16 * 16];     // Mp[7][D][DP] | Wt[4][D][DP] (= tabs[64 D, 64 D + 11 D DP))
     float escale[16];            // 2^-fK_i of the Ke columns
     unsigned long long *aggw;    // [tiles][D] {value, 1}: zero-carry tile aggregates (zeroed before the launch)
     unsigned long long *inclw;   // [blocks][C][D] {value, 1}: state after block-end tiles (k % 32 == 31)
@@ -94,7 +119,7 @@ struct LbArgs {
 };
 
 // ---- table layout shared by host and device (floats) ----
-// Es[64][D] | Mp[7][D][DP] (M^(2^b)) | Wt[4][D][DP] (M^(32 w)) | Gl[LT][32] (M^l, lane-minor; D <= 8 only)
+// Ep[32][D][2] (E[2q][d], E[2q+1][d] pairs) | Mp[7][D][DP] (M^(2^b)) | Wt[4][D][DP] (M^(32 w)) | Gl[LT][32] (M^l, lane-minor; D <= 8 only)
 __host__ __device__ constexpr int lb_de(int D) { return D <= 8 ? 8 : 16; }
 __host__ __device__ constexpr int lb_dp(int D) { return (D + 3) & ~3; }
 __host__ __device__ constexpr int lb_has_gl(int D) { return D <= 8; }
@@ -108,33 +133,25 @@ __host__ __device__ constexpr int lb_off_gl(int D) { return 64 * D + 11 * D * lb
 __host__ __device__ constexpr uint32_t lb_bhi(int a) { return a == 0 ? 0u : 20480u + (uint32_t)(a - 1) * 16384u; }
 __host__ __device__ constexpr uint32_t lb_blo(int a) { return lb_bhi(a) + (a == 0 ? 10240u : 8192u); }
 __host__ __device__ constexpr uint32_t lb_bbytes(int K) { return lb_bhi((K + 63) / 64); }
-// state-term operands: K = 3 DE fp16 per row ([s_hi | s_lo | s_hi]), padded to 16; no-swizzle K-major
-__host__ __device__ constexpr int lb_ks(int D) { return (3 * lb_de(D) + 15) / 16 * 16; }
-__host__ __device__ constexpr uint32_t lb_sbo(int D) { return (uint32_t)lb_ks(D) / 8u * 128u; }
-__host__ __device__ constexpr uint32_t lb_s_off(int D, int r, int k) {
-    return (uint32_t)(r >> 3) * lb_sbo(D) + (uint32_t)(k >> 3) * 128u + (uint32_t)(r & 7) * 16u + (uint32_t)(k & 7) * 2u;
-}
 
 struct LbLayout {
-    uint32_t opBytes, bBytes, sopBytes;
-    uint32_t bimg, op, raw, tabs, sop, bs, stg, misc, bars;
+    uint32_t opBytes, bBytes;
+    uint32_t bimg, op, raw, tabs, ring, stg, misc, bars;
     uint32_t total;
     __host__ __device__ LbLayout(int W, int K, int D, int nop) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
         bBytes = lb_bbytes(K);
-        sopBytes = 128u * (uint32_t)lb_ks(D) * 2u;
         bimg = 0;
         op = bimg + bBytes;
         raw = op + 2u * (uint32_t)nop * opBytes;
         const uint32_t rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         tabs = raw + rawBytes;
-        sop = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [2 groups] state operands
-        bs = sop + 2u * sopBytes;                                         // state-term B
-        stg = bs + 64u * (uint32_t)lb_ks(D) * 2u;
-        misc = stg + 8u * 32u * CT_STG_PITCH;
-        // misc: Tw[2][4][D], cb[NC][D] f32; scl[RING] f32, red[8] f32, stag[RING] i32
-        bars = (misc + 4u * (uint32_t)((8 + LB_NC) * D) + 4u * (2 * LB_RING + 8) + 15u) & ~15u;
-        total = bars + 48 * 8 + 16 + 1024;  // + alignment slack (42 barriers + TMEM slot)
+        ring = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [NL][D][128] row prefixes
+        stg = ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS);  // [LB_EG groups][4 warps][32 rows] staging
+        misc = stg + 4u * LB_EG * 32u * CT_STG_PITCH;
+        // misc: Tw[2][4][D], cb[NC][D] f32; scl[RING] f32, rsc[NL] f32, red[8] f32, stag[RING] i32
+        bars = (misc + 4u * (uint32_t)((8 + LB_NC) * D) + 4u * (2 * LB_RING + LB_NL + 8) + 15u) & ~15u;
+        total = bars + 48 * 8 + 16 + 1024;  // + alignment slack (35 barriers + TMEM slot)
     }
 };
 
@@ -155,8 +172,8 @@ __device__ __forceinline__ void st_word(unsigned long long *p, float v) {
 template <int D>
 __device__ __forceinline__ void wait_words(const unsigned long long *p, float (&v)[D]) {
     unsigned long long w[D];
-    const unsigned long long t0 = ctd::gtimer();
-    unsigned ns = 32;
+    unsigned long long t0 = 0;
+    unsigned ns = 32, it = 0;
     for (;;) {
 #pragma unroll
         for (int d = 0; d < D; ++d) w[d] = ld_word(p + d);
@@ -165,8 +182,12 @@ __device__ __forceinline__ void wait_words(const unsigned long long *p, float (&
         for (int d = 0; d < D; ++d) ok = ok && (w[d] >> 32) != 0;
         if (ok) break;
         __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : 256;
-        if (ctd::gtimer() - t0 > 10000000000ull) __trap();
+        ns = ns < 128 ? 2 * ns : 128;
+        if ((++it & 63u) == 0) {
+            const unsigned long long t = ctd::gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 10000000000ull) __trap();
+        }
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) v[d] = __uint_as_float((unsigned)w[d]);
@@ -204,6 +225,67 @@ __device__ __forceinline__ void lt_mv4(float (&out)[D], const float *m, const fl
     }
 }
 
+
+// Wait for an mbarrier phase: non-blocking probes with a nanosleep back-off
+// from 32 ns up to MAXNS, the watchdog clock read every 64 probes only. Every
+// probe costs issue slots the working warps need (try_wait's suspend returns
+// whenever any barrier of the CTA changes), so each role has ONE waiting
+// thread and fans out through a named barrier (blocked in hardware).
+template <unsigned MAXNS>
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    if (wptc::mbar_test(bar, parity)) return;
+    unsigned ns = 32, it = 0;
+    unsigned long long t0 = 0;
+    while (!wptc::mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < MAXNS ? 2 * ns : MAXNS;
+        if ((++it & 63u) == 0) {
+            const unsigned long long t = ctd::gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 10000000000ull) __trap();
+        }
+    }
+}
+
+// (a0, a1) += (e0, e1) * s as one packed fp32x2 FMA (FFMA2)
+__device__ __forceinline__ void ffma2(float &a0, float &a1, float e0, float e1, float s) {
+    unsigned long long acc = (unsigned long long)__float_as_uint(a0) | ((unsigned long long)__float_as_uint(a1) << 32);
+    const unsigned long long ev = (unsigned long long)__float_as_uint(e0) | ((unsigned long long)__float_as_uint(e1) << 32);
+    const unsigned long long sv = (unsigned long long)__float_as_uint(s) | ((unsigned long long)__float_as_uint(s) << 32);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ev), "l"(sv));
+    a0 = __uint_as_float((unsigned)acc);
+    a1 = __uint_as_float((unsigned)(acc >> 32));
+}
+
+// s += M^lane V (M^l for l = lane < 32): lane-minor table Gl for D <= 8, else
+// five conditional squarings-table steps (Mp[b] = M^(2^b))
+template <int D>
+__device__ __forceinline__ void add_mlane(float (&s)[D], float (&V)[D], const float *Mp, const float *Gl, int lane) {
+    constexpr int DP = lb_dp(D);
+    if constexpr (lb_has_gl(D)) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            float acc = s[r];
+#pragma unroll
+            for (int q = 0; q < lt_nj(r); ++q) acc = fmaf(Gl[(lt_off(r) + q) * 32 + lane], V[q], acc);
+            s[r] = acc;
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+            float t[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) t[d] = 0.f;
+            lt_mv4<D>(t, Mp + b * D * DP, V);
+            if ((lane >> b) & 1) {
+#pragma unroll
+                for (int d = 0; d < D; ++d) V[d] = t[d];
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) s[d] += V[d];
+    }
+}
 }  // namespace lbd
 
 template <int D, int NOP>
@@ -211,9 +293,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     static_assert(D >= 2 && D <= 16 && (D % 2) == 0, "2..8 sections");
     static_assert(NOP == 2 || NOP == 3, "two or three fp16 operand stages");
     static_assert(LB_NA * LB_NS <= 512, "TMEM columns");
-    constexpr int DE = lb_de(D);
+    static_assert(28 + 2 * LB_NL <= 48, "barrier slots");
     constexpr int DP = lb_dp(D);
-    constexpr int KS = lb_ks(D);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -222,17 +303,24 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     unsigned char *bimg = smem + lay.bimg;
     unsigned char *op = smem + lay.op;
     float *tabs = reinterpret_cast<float *>(smem + lay.tabs);
-    const float *Es = tabs;
+#if LB_M_CONST
+    const float *Mp = a.Mpw;
+    const float *Wt = a.Mpw + 7 * D * DP;
+#else
     const float *Mp = tabs + lb_off_mp(D);
     const float *Wt = tabs + lb_off_wt(D);
+#endif
+#if !LB_E_CONST
+    const float4 *Ep = reinterpret_cast<const float4 *>(tabs);  // [32][D / 2]: E pairs of two states
+#endif
     const float *Gl = tabs + lb_off_gl(D);
-    unsigned char *sop = smem + lay.sop;  // [2 groups][128 rows][KS] fp16 state operands
-    unsigned char *bsi = smem + lay.bs;   // [64 rows][KS] fp16 state-term B
+    float *ring = reinterpret_cast<float *>(smem + lay.ring);  // [NL][D][128] row prefixes (zero carry)
     unsigned char *stg = smem + lay.stg;
-    float *Tw = reinterpret_cast<float *>(smem + lay.misc);  // [2 groups][4][D] warp totals
+    float *Tw = reinterpret_cast<float *>(smem + lay.misc);  // [2 parities][4][D] scan warp totals
     float *cb = Tw + 8 * D;                                  // [NC][D] carry-in ring
     float *scl = cb + LB_NC * D;                             // [RING] tile scales
-    float *red = scl + LB_RING;                              // [8]
+    float *rsc = scl + LB_RING;                              // [NL] tile scales of the ring slots
+    float *red = rsc + LB_NL;                                // [8]
     int *stag = reinterpret_cast<int *>(red + 8);            // [RING] local tile index of scl[]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 48);
@@ -241,18 +329,17 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     do {                                                                              \
         if (a.trace) a.trace[(long long)(tile) * LB_TRACE_EV + (ev)] = ctd::gtimer(); \
     } while (0)
-    // barriers: OP_FULL / OP_EMPTY x 3; E_READY / S_READY / ACC_FULL / ACC_EMPTY x 6;
-    // C_READY / C_EMPTY x 4; RAW full / empty
+    // barriers: OP_FULL / OP_EMPTY x 3; E_READY / ACC_EMPTY x 6; C_READY / C_EMPTY x 4;
+    // RAW full; L_FULL / L_EMPTY x 4
 #define OPF(s) (bar0 + 8u * (uint32_t)(0 + (s)))
 #define OPE(s) (bar0 + 8u * (uint32_t)(3 + (s)))
 #define EFL(s) (bar0 + 8u * (uint32_t)(6 + (s)))
-#define SRD(s) (bar0 + 8u * (uint32_t)(12 + (s)))
-#define ACF(s) (bar0 + 8u * (uint32_t)(18 + (s)))
-#define ACE(s) (bar0 + 8u * (uint32_t)(24 + (s)))
-#define CRD(s) (bar0 + 8u * (uint32_t)(30 + (s)))
-#define CEM(s) (bar0 + 8u * (uint32_t)(34 + (s)))
-#define RWF (bar0 + 8u * 38u)
-#define RWE (bar0 + 8u * 39u)
+#define ACE(s) (bar0 + 8u * (uint32_t)(12 + (s)))
+#define CRD(s) (bar0 + 8u * (uint32_t)(18 + (s)))
+#define CEM(s) (bar0 + 8u * (uint32_t)(22 + (s)))
+#define RWF (bar0 + 8u * 26u)
+#define LFL(s) (bar0 + 8u * (uint32_t)(28 + (s)))
+#define LEM(s) (bar0 + 8u * (uint32_t)(28 + LB_NL + (s)))
 
     if (warp == 0) wptc::tmem_alloc(wptc::smem_u32(tmem_slot), 512);
     if (tid == 32) {
@@ -262,23 +349,23 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
         }
         for (int s = 0; s < LB_NA; ++s) {
             wptc::mbar_init(EFL(s), 1);
-            wptc::mbar_init(SRD(s), CT_ROWS);
-            wptc::mbar_init(ACF(s), 1);
             wptc::mbar_init(ACE(s), CT_ROWS);
+
         }
         for (int s = 0; s < LB_NC; ++s) {
             wptc::mbar_init(CRD(s), 1);
             wptc::mbar_init(CEM(s), CT_ROWS);
         }
+        for (int s = 0; s < LB_NL; ++s) {
+            wptc::mbar_init(LFL(s), CT_ROWS);
+            wptc::mbar_init(LEM(s), CT_ROWS);
+        }
         wptc::mbar_init(RWF, 1);
-        wptc::mbar_init(RWE, 1);
         wptc::mbar_fence_init();
     }
     for (int i = tid; i < (int)(lay.bBytes / 16); i += LB_THREADS)
         reinterpret_cast<uint4 *>(bimg)[i] = reinterpret_cast<const uint4 *>(a.Bimg)[i];
     for (int i = tid; i < lb_tab_floats(D); i += LB_THREADS) tabs[i] = a.stabs[i];
-    for (int i = tid; i < 64 * KS * 2 / 16; i += LB_THREADS)
-        reinterpret_cast<uint4 *>(bsi)[i] = reinterpret_cast<const uint4 *>(a.Bsimg)[i];
     if (tid < LB_RING) stag[tid] = -1;
     wptc::fence_proxy_async_smem();
     wptc::fence_before_sync();
@@ -289,96 +376,36 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     const int ntiles = first < a.total_tiles ? (int)((a.total_tiles - 1 - first) / stride + 1) : 0;
 
     if (warp == 0) {
-        // ================= MMA issuer: main(i), then state(i - LAG) =================
+        // ================= MMA issuer: the main GEMM of every tile, in tile order =================
         if (lane == 0) {
             const uint32_t id_e = wptc::idesc_f16(128, LB_NS);  // first K atom: [g | Ke | 0]
-            const uint32_t id_g = wptc::idesc_f16(128, 64);     // other atoms, state term
+            const uint32_t id_g = wptc::idesc_f16(128, 64);     // other atoms
             const uint32_t op0 = wptc::smem_u32(op), b0 = wptc::smem_u32(bimg);
-            const uint32_t sop0 = wptc::smem_u32(sop), bs0 = wptc::smem_u32(bsi);
-            // issue whichever is ready: the next main GEMM (operands converted, a
-            // free accumulator stage) or the next state GEMM (state operand
-            // written); each kind in tile order
-            int im = 0, is = 0;
-            unsigned idle = 0;
-            const unsigned long long t0 = ctd::gtimer();
-            while (is < ntiles) {
-                bool done = false;
-                if (im < ntiles && im - is < LB_NA) {
-                    const int so = im % NOP;
-                    const int sa = im % LB_NA;
-                    if (wptc::mbar_test(OPF(so), (uint32_t)((im / NOP) & 1)) &&
-                        wptc::mbar_test(ACE(sa), (uint32_t)((im / LB_NA) & 1) ^ 1u)) {
-                        wptc::fence_after_sync();
-                        LBTR(first + (long long)im * stride, 2);
-                        const uint32_t dm = tmem + (uint32_t)LB_NS * sa;
-                        const uint32_t ahi = op0 + (2u * so) * lay.opBytes, alo = ahi + lay.opBytes;
-                        const uint64_t ah0 = ctd::desc_sw128(ahi), al0 = ctd::desc_sw128(alo);
+            for (int im = 0; im < ntiles; ++im) {
+                const int so = im % NOP;
+                const int sa = im % LB_NA;
+                wptc::mbar_wait(OPF(so), (uint32_t)((im / NOP) & 1));
+                wptc::mbar_wait(ACE(sa), (uint32_t)((im / LB_NA) & 1) ^ 1u);
+                wptc::fence_after_sync();
+                LBTR(first + (long long)im * stride, 2);
+                const uint32_t dm = tmem + (uint32_t)LB_NS * sa;
+                const uint32_t ahi = op0 + (2u * so) * lay.opBytes, alo = ahi + lay.opBytes;
+                const uint64_t ah0 = ctd::desc_sw128(ahi), al0 = ctd::desc_sw128(alo);
 #pragma unroll 1
-                        for (int kk = 0; kk < nk; ++kk) {
-                            const uint64_t ka = 2u * kk;  // +32 B per K step, across rows (Hankel)
-                            const int at = kk >> 2;
-                            const uint32_t sub = 32u * (uint32_t)(kk & 3);
-                            const uint64_t bh = ctd::desc_sw128(b0 + lb_bhi(at) + sub);
-                            const uint64_t bl = ctd::desc_sw128(b0 + lb_blo(at) + sub);
-                            const uint32_t id = at == 0 ? id_e : id_g;
-                            wptc::mma_f16(dm, ah0 + ka, bh, id, kk > 0);  // x_hi g_hi
-                            wptc::mma_f16(dm, ah0 + ka, bl, id, 1u);      // x_hi g_lo
-                            wptc::mma_f16(dm, al0 + ka, bh, id, 1u);      // x_lo g_hi
-                        }
-                        wptc::mma_commit(OPE(so));
-                        wptc::mma_commit(EFL(sa));
-                        LBTR(first + (long long)im * stride, 3);
-                        ++im;
-                        done = true;
-                    }
+                for (int kk = 0; kk < nk; ++kk) {
+                    const uint64_t ka = 2u * kk;  // +32 B per K step, across rows (Hankel)
+                    const int at = kk >> 2;
+                    const uint32_t sub = 32u * (uint32_t)(kk & 3);
+                    const uint64_t bh = ctd::desc_sw128(b0 + lb_bhi(at) + sub);
+                    const uint64_t bl = ctd::desc_sw128(b0 + lb_blo(at) + sub);
+                    const uint32_t id = at == 0 ? id_e : id_g;
+                    wptc::mma_f16(dm, ah0 + ka, bh, id, kk > 0);  // x_hi g_hi
+                    wptc::mma_f16(dm, ah0 + ka, bl, id, 1u);      // x_hi g_lo
+                    wptc::mma_f16(dm, al0 + ka, bh, id, 1u);      // x_lo g_hi
                 }
-                if (is < im) {
-                    const int sa = is % LB_NA;
-                    if (wptc::mbar_test(SRD(sa), (uint32_t)((is / LB_NA) & 1))) {
-                        // state term of tile is: [s_hi | s_lo | s_hi] x [E_hi; E_hi; E_lo]
-                        wptc::fence_after_sync();
-                        const uint32_t dm = tmem + (uint32_t)LB_NS * sa;
-                        const uint32_t sa0 = sop0 + (uint32_t)(is & 1) * lay.sopBytes;
-#pragma unroll
-                        for (int kk = 0; kk < KS / 16; ++kk)
-                            wptc::mma_f16(dm, c3d::desc_sbo(sa0 + 256u * kk, lb_sbo(D)),
-                                          c3d::desc_sbo(bs0 + 256u * kk, lb_sbo(D)), id_g, 1u);
-                        wptc::mma_commit(ACF(sa));
-                        ++is;
-                        done = true;
-                    }
-                }
-                if (!done) {
-                    __nanosleep(20);
-                    if ((++idle & 1023u) == 0 && ctd::gtimer() - t0 > 10000000000ull) __trap();
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ================= bulk-copy producer: fp32 window -> smem =================
-        if (lane == 0) {
-            const uint32_t raw0 = wptc::smem_u32(smem + lay.raw);
-            for (int i = 0; i < ntiles; ++i) {
-                wptc::mbar_wait_sleep<256>(RWE, (uint32_t)(i & 1) ^ 1u);
-                const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
-                const uint32_t bytes = (uint32_t)(4 * (g.hi - g.lo));
-                if (bytes > 0) {
-                    c3d::arrive_tx(RWF, bytes);
-                    const float *src = a.x + g.c * a.ldx + g.lo;
-                    const uint32_t dst = raw0 + 4u * (uint32_t)(g.lo - g.start);
-                    for (uint32_t o = 0; o < bytes; o += 16384u) {
-                        const uint32_t nb = bytes - o < 16384u ? bytes - o : 16384u;
-                        c3d::bulk_g2s(dst + o, reinterpret_cast<const unsigned char *>(src) + o, nb, RWF);
-                    }
-                } else {
-                    ctd::arrive(RWF);
-                }
-                const long long nt = first + (long long)(i + 2) * stride;
-                if (i + 2 < ntiles) {
-                    const c3d::Win g2 = c3d::win(nt, a.C, a.N, a.H, a.W, a.vec_x);
-                    const uint32_t b2 = (uint32_t)(4 * (g2.hi - g2.lo));
-                    if (b2 > 0) ctd::prefetch_l2(a.x + g2.c * a.ldx + g2.lo, b2);
-                }
+                wptc::mma_commit(OPE(so));
+                wptc::mma_commit(EFL(sa));
+                LBTR(first + (long long)im * stride, 3);
             }
         }
     } else if (warp >= 2 && warp < 2 + LB_CONV / 32) {
@@ -387,13 +414,42 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
         const int cw = ct >> 5;
         const int nq = a.W / 4;
         const float4 *raw4 = reinterpret_cast<const float4 *>(smem + lay.raw);
+        const uint32_t raw0 = wptc::smem_u32(smem + lay.raw);
+        // thread 0 is also the bulk-copy producer of the (single) fp32 window buffer:
+        // tile i + 1 is requested as soon as every converter holds tile i in registers
+        auto issue_window = [&](int i) {
+            const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
+            const uint32_t bytes = (uint32_t)(4 * (g.hi - g.lo));
+            if (bytes > 0) {
+                c3d::arrive_tx(RWF, bytes);
+                const float *src = a.x + g.c * a.ldx + g.lo;
+                const uint32_t dst = raw0 + 4u * (uint32_t)(g.lo - g.start);
+                for (uint32_t o = 0; o < bytes; o += 16384u) {
+                    const uint32_t nb = bytes - o < 16384u ? bytes - o : 16384u;
+                    c3d::bulk_g2s(dst + o, reinterpret_cast<const unsigned char *>(src) + o, nb, RWF);
+                }
+            } else {
+                ctd::arrive(RWF);
+            }
+            if (i + 2 < ntiles) {
+                const c3d::Win g2 = c3d::win(first + (long long)(i + 2) * stride, a.C, a.N, a.H, a.W, a.vec_x);
+                const uint32_t b2 = (uint32_t)(4 * (g2.hi - g2.lo));
+                if (b2 > 0) ctd::prefetch_l2(a.x + g2.c * a.ldx + g2.lo, b2);
+            }
+        };
+        if (ct == 0 && ntiles > 0) issue_window(0);
         for (int i = 0; i < ntiles; ++i) {
             const int s = i % NOP;
             const uint32_t par = (uint32_t)((i / NOP) & 1);
             const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
             const float *xr = a.x + g.c * a.ldx;
             const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
+#if LB_GROUP_WAIT
+            if (ct == 0) lbd::bar_wait<256>(RWF, (uint32_t)(i & 1));
+            ctd::named_sync(4, LB_CONV);
+#else
             wptc::mbar_wait_sleep<256>(RWF, (uint32_t)(i & 1));
+#endif
             if (ct == 0) LBTR(first + (long long)i * stride, 0);
             float4 v[LB_QMAX];
             float m = 0.f;
@@ -428,14 +484,21 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
             if (lane == 0) red[cw] = __uint_as_float(mb);
             ctd::named_sync(1, LB_CONV);
-            if (ct == 0) ctd::arrive(RWE);  // the window is in registers: free it
+            if (ct == 0 && i + 1 < ntiles) issue_window(i + 1);  // the window is in registers: refill it
+#if LB_GROUP_WAIT
+            if (ct == 0) lbd::bar_wait<256>(OPE(s), par ^ 1u);
+#endif
             float tmax = red[0];
 #pragma unroll
             for (int w = 1; w < LB_CONV / 32; ++w) tmax = fmaxf(tmax, red[w]);
             int ex = 0;
             if (tmax > 0.f) frexpf(tmax, &ex);
             const float sc = ldexpf(1.f, tmax > 0.f ? 14 - ex : 0);
+#if LB_GROUP_WAIT
+            ctd::named_sync(5, LB_CONV);
+#else
             wptc::mbar_wait_sleep<1024>(OPE(s), par ^ 1u);
+#endif
             unsigned char *ohi = op + (2 * s) * lay.opBytes, *olo = ohi + lay.opBytes;
 #pragma unroll
             for (int j = 0; j < LB_QMAX; ++j) {
@@ -469,14 +532,14 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                 LBTR(first + (long long)i * stride, 1);
             }
         }
-    } else if (warp == 7) {
-        // ================= look-back: carry-in of each tile =================
-        for (int i = 0; i < ntiles; ++i) {
+    } else if (warp == 1 || warp == 7) {
+        // ================= look-back (warp 1: even, warp 7: odd local tiles): carry-in of each tile =================
+        for (int i = warp == 1 ? 0 : 1; i < ntiles; i += 2) {
             const int sc4 = i % LB_NC;
             const long long tile = first + (long long)i * stride;
             const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
             const long long k = (long long)((unsigned long long)tile / (unsigned long long)a.C);
-            wptc::mbar_wait_sleep<512>(CEM(sc4), (uint32_t)((i / LB_NC) & 1) ^ 1u);  // slot read by the row group
+            wptc::mbar_wait_sleep<512>(CEM(sc4), (uint32_t)((i / LB_NC) & 1) ^ 1u);  // slot read by the epilogue
             if (lane == 0) LBTR(tile, 4);
             // c_k = sum_{l < j} MT^l agg(k-1-l) + MT^j incl(kb - 1)
             const long long kb = k & ~(long long)(LB_BLK - 1);
@@ -484,9 +547,6 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             float w[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) w[d] = 0.f;
-            // predecessors publish roughly in tile order: the nearest one first
-            if (lane == 0 && j > 0) lbd::wait_word(a.aggw + ((k - 1) * a.C + c) * D + (D - 1));
-            __syncwarp();
             if (lane < j || (lane == j && kb > 0)) {
                 const unsigned long long *src = lane < j ? a.aggw + ((k - 1 - lane) * a.C + c) * D
                                                          : a.inclw + ((kb / LB_BLK - 1) * a.C + c) * D;
@@ -528,32 +588,39 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             }
             __syncwarp();
         }
-    } else {
-        // ================= row groups (warps 8-11: even, 12-15: odd local tiles) =================
-        const int grp = (warp - 8) >> 2;
+    } else if (warp < 12) {
+        // ================= scan (warps 8-11): row prefixes at zero carry, tile aggregates =================
         const int wq = warp & 3;
         const int row = 32 * wq + lane;
         const uint32_t trow = (uint32_t)(32 * wq) << 16;
-        unsigned char *mystg = stg + (size_t)(grp * 4 + wq) * 32 * CT_STG_PITCH;
-        unsigned char *mysop = sop + (size_t)grp * lay.sopBytes;
-        float *Tg = Tw + grp * 4 * D;  // this group's warp totals
-        // scan of local tile i: zero-carry prefix s (row), warp start V, tile scale;
-        // publishes the tile aggregate
-        auto scan_tile = [&](int i, float (&s)[D], float (&V)[D], float &sci) {
+#pragma unroll 1
+        for (int i = 0; i < ntiles; ++i) {
             const int sa = i % LB_NA;
-            const uint32_t para = (uint32_t)((i / LB_NA) & 1);
             const long long tile = first + (long long)i * stride;
-            wptc::mbar_wait_sleep<256>(EFL(sa), para);
-            wptc::fence_after_sync();
-            float ev[16];
-            ctd::tmem_ld16(tmem + (uint32_t)LB_NS * sa + 64u + trow, ev);
-            wptc::tmem_wait_ld();
+            const int sl = i % LB_NL;
+#if LB_GROUP_WAIT
+            if (row == 0) {
+                lbd::bar_wait<128>(EFL(sa), (uint32_t)((i / LB_NA) & 1));
+                for (int spins = 0; *reinterpret_cast<volatile int *>(stag + (i % LB_RING)) != i; ++spins) {
+                    __nanosleep(64);
+                    if (spins > (1 << 28)) __trap();
+                }
+            }
+            ctd::named_sync(6, 128);
+#else
+            wptc::mbar_wait_sleep<128>(EFL(sa), (uint32_t)((i / LB_NA) & 1));
             for (int spins = 0; *reinterpret_cast<volatile int *>(stag + (i % LB_RING)) != i; ++spins) {
                 __nanosleep(32);
                 if (spins > (1 << 28)) __trap();
             }
             __threadfence_block();
-            sci = scl[i % LB_RING];
+#endif
+            wptc::fence_after_sync();
+            if (row == 0) LBTR(tile, 8);
+            float ev[16];
+            ctd::tmem_ld16(tmem + (uint32_t)LB_NS * sa + 64u + trow, ev);
+            wptc::tmem_wait_ld();
+            const float sci = scl[i % LB_RING];
             const float inv_sc = 1.f / sci;
             float P[D];
 #pragma unroll
@@ -568,17 +635,20 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                 if (lane >= off) lbd::lt_mv4<D>(P, Mp + b * D * DP, prev);
             }
             // exclusive: state entering the row from the warp start (zero carry)
+            float s[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) {
                 const float u = __shfl_up_sync(0xffffffffu, P[d], 1);
                 s[d] = lane == 0 ? 0.f : u;
             }
+            float *Tg = Tw + (i & 1) * 4 * D;  // double-buffered: one barrier per tile
             if (lane == 31) {
 #pragma unroll
                 for (int d = 0; d < D; ++d) Tg[wq * D + d] = P[d];
             }
-            ctd::named_sync(3 + grp, 128);
+            ctd::named_sync(3, 128);
             // Z_w: state at the warp start (zero carry at the tile start)
+            float V[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) V[d] = 0.f;
 #pragma unroll 1
@@ -599,96 +669,60 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
 #pragma unroll
                 for (int d = 0; d < D; ++d) lbd::st_word(a.aggw + tile * D + d, agg[d]);
             }
-            ctd::named_sync(3 + grp, 128);  // Tg is rewritten by the group's next tile
-            if (row == 0) LBTR(tile, 6);
-        };
-        // software pipeline: the scan of the group's next tile runs before this
-        // tile waits for its carry, so aggregates are published early and the
-        // look-back latency overlaps a scan
-        float sN[D], VN[D], sciN = 1.f;
-#pragma unroll 1
-        for (int it = grp; it < ntiles + 2; it += 2) {
-            float s[D], V[D];
+            // L_m = s + M^lane Z_w: the state entering row m at zero carry from the tile start
+            lbd::add_mlane<D>(s, V, Mp, Gl, lane);
+            if (row == 0) LBTR(tile, 12);
+            // only now (the aggregate is out) wait for the ring slot
+            wptc::mbar_wait_sleep<256>(LEM(sl), (uint32_t)((i / LB_NL) & 1) ^ 1u);
 #pragma unroll
-            for (int d = 0; d < D; ++d) s[d] = sN[d], V[d] = VN[d];
-            const float sci = sciN;
-            if (it < ntiles) scan_tile(it, sN, VN, sciN);
-            const int i = it - 2;
-            if (i < grp) continue;
-            const int sa = i % LB_NA;
-            const uint32_t para = (uint32_t)((i / LB_NA) & 1);
-            const int sc4 = i % LB_NC;
+            for (int d = 0; d < D; ++d) ring[(sl * D + d) * CT_ROWS + row] = s[d];
+            if (row == 0) rsc[sl] = sci;
+            ctd::arrive(LFL(sl));
+            if (row == 0) LBTR(tile, 6);
+        }
+    } else {
+        // ================= epilogue (warps 12-15: even, 16-19: odd local tiles) =================
+        // s_m = L_m + M^m c, TMEM + E s_m -> y
+        const int grp = LB_EG > 1 ? (warp - 12) >> 2 : 0;
+        const int wq = warp & 3;
+        const int row = 32 * wq + lane;
+        const uint32_t trow = (uint32_t)(32 * wq) << 16;
+        unsigned char *mystg = stg + (size_t)(4 * grp + wq) * 32 * CT_STG_PITCH;
+#pragma unroll 1
+        for (int i = grp; i < ntiles; i += LB_EG) {
+            const int sa = i % LB_NA, sl = i % LB_NL, sc4 = i % LB_NC;
             const long long tile = first + (long long)i * stride;
             const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
             const long long n0 = (long long)((unsigned long long)tile / (unsigned long long)a.C) * (long long)CT_TOUT;
-            wptc::mbar_wait_sleep<256>(CRD(sc4), (uint32_t)((i / LB_NC) & 1));
+#if LB_GROUP_WAIT
+            if (row == 0) {
+                lbd::bar_wait<128>(LFL(sl), (uint32_t)((i / LB_NL) & 1));
+                lbd::bar_wait<128>(CRD(sc4), (uint32_t)((i / LB_NC) & 1));
+            }
+            ctd::named_sync(7 + grp, 128);
+#else
+            wptc::mbar_wait_sleep<128>(LFL(sl), (uint32_t)((i / LB_NL) & 1));
+            wptc::mbar_wait_sleep<128>(CRD(sc4), (uint32_t)((i / LB_NC) & 1));
+#endif
+            float s[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) s[d] = ring[(sl * D + d) * CT_ROWS + row];
+            const float sci = rsc[sl];
+            ctd::arrive(LEM(sl));
+            if (row == 0) LBTR(tile, 10);
             if (row == 0) LBTR(tile, 9);
             {
-                // s_m = L_m + M^lane (Z_w + M^(32 w) c)
-                float cin[D];
+                // s_m = L_m + M^lane (M^(32 w) c)
+                float cin[D], V[D];
 #pragma unroll
-                for (int d = 0; d < D; ++d) cin[d] = cb[sc4 * D + d];
+                for (int d = 0; d < D; ++d) cin[d] = cb[sc4 * D + d], V[d] = 0.f;
                 ctd::arrive(CEM(sc4));
                 lbd::lt_mv4<D>(V, Wt + wq * D * DP, cin);
-                if constexpr (lb_has_gl(D)) {
-#pragma unroll
-                    for (int r = 0; r < D; ++r) {
-                        float acc = s[r];
-#pragma unroll
-                        for (int q = 0; q < lt_nj(r); ++q) acc = fmaf(Gl[(lt_off(r) + q) * 32 + lane], V[q], acc);
-                        s[r] = acc;
-                    }
-                } else {
-#pragma unroll
-                    for (int b = 0; b < 5; ++b) {
-                        float t[D];
-#pragma unroll
-                        for (int d = 0; d < D; ++d) t[d] = 0.f;
-                        lbd::lt_mv4<D>(t, Mp + b * D * DP, V);
-                        if ((lane >> b) & 1) {
-#pragma unroll
-                            for (int d = 0; d < D; ++d) V[d] = t[d];
-                        }
-                    }
-#pragma unroll
-                    for (int d = 0; d < D; ++d) s[d] += V[d];
-                }
+                lbd::add_mlane<D>(s, V, Mp, Gl, lane);
             }
-            // state operand [s_hi | s_lo | s_hi] x tile scale x 2^(fB - fE); a row that
-            // would overflow fp16 sends zeros and takes the CUDA-core path below
-            bool ovf = false;
-            {
-                const float f = sci * a.st_mul;
-                float v[D];
-#pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    v[d] = s[d] * f;
-                    ovf = ovf || !(fabsf(v[d]) < 32768.f);
-                }
-#pragma unroll
-                for (int k8 = 0; k8 < KS / 8; ++k8) {
-                    uint32_t hw[4];
-#pragma unroll
-                    for (int t2 = 0; t2 < 4; ++t2) {
-                        __half pr[2];
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int k = 8 * k8 + 2 * t2 + u;
-                            const int part = k / DE, d = k % DE;  // 0: hi, 1: lo, 2: hi, 3: pad
-                            const float val = (d < D && part < 3 && !ovf) ? v[d < D ? d : 0] : 0.f;
-                            const __half hi = __float2half_rn(val);
-                            pr[u] = part == 1 ? __float2half_rn(val - __half2float(hi)) : hi;
-                        }
-                        hw[t2] = (uint32_t)__half_as_ushort(pr[0]) | ((uint32_t)__half_as_ushort(pr[1]) << 16);
-                    }
-                    *reinterpret_cast<uint4 *>(mysop + lb_s_off(D, row, 8 * k8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                }
-            }
-            wptc::fence_proxy_async_smem();
-            ctd::arrive(SRD(sa));
-            wptc::mbar_wait_sleep<256>(ACF(sa), para);
+            if (row == 0) LBTR(tile, 11);
+            wptc::mbar_wait(EFL(sa), (uint32_t)((i / LB_NA) & 1));  // completed before the scan: ordering only
             wptc::fence_after_sync();
-            if (row == 0) LBTR(tile, 10);
             const float osc = a.out_scale / sci;
             const uint32_t tbase = tmem + (uint32_t)LB_NS * sa + trow;
             float *yr = a.y + c * a.ldy + n0;
@@ -700,30 +734,32 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                 float o16[16];
                 ctd::tmem_ld16(tbase + 16u * ch, o16);
                 wptc::tmem_wait_ld();
+                if (ch == 0 && row == 0) LBTR(tile, 13);
                 if (ch == 3) {
                     wptc::fence_before_sync();
                     ctd::arrive(ACE(sa));  // the accumulator has been read: free it
                 }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) o16[j] *= osc;
-                if (__any_sync(0xffffffffu, ovf)) {
-                    // rare: rows whose state operand would overflow fp16 add E s here
-#pragma unroll 1
-                    for (int j = 0; j < 16; ++j) {
-                        const float *e = Es + (16 * ch + j) * D;
-                        float acc = 0.f;
 #pragma unroll
-                        for (int d = 0; d < D; ++d) acc = fmaf(e[d], s[d], acc);
-                        if (ovf) reinterpret_cast<float *>(mystg + lane * CT_STG_PITCH + 64 * hh)[j] = acc;
-                        else reinterpret_cast<float *>(mystg + lane * CT_STG_PITCH + 64 * hh)[j] = 0.f;
-                    }
-                    float4 *add = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
+                for (int pp = 0; pp < 8; ++pp)
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const float4 t = add[q4];
-                        o16[4 * q4] += t.x, o16[4 * q4 + 1] += t.y, o16[4 * q4 + 2] += t.z, o16[4 * q4 + 3] += t.w;
+                    for (int d2 = 0; d2 < D / 2; ++d2) {
+#if LB_E_CONST
+                        const float4 e = a.Ep[(8 * ch + pp) * (D / 2) + d2];  // E[p][2 d2 .. +1], E[p + 1][..]
+#else
+                        const float4 e = Ep[(8 * ch + pp) * (D / 2) + d2];
+#endif
+#if LB_FFMA2
+                        lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.x, e.y, s[2 * d2]);
+                        lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.z, e.w, s[2 * d2 + 1]);
+#else
+                        o16[2 * pp] = fmaf(e.x, s[2 * d2], o16[2 * pp]);
+                        o16[2 * pp + 1] = fmaf(e.y, s[2 * d2], o16[2 * pp + 1]);
+                        o16[2 * pp] = fmaf(e.z, s[2 * d2 + 1], o16[2 * pp]);
+                        o16[2 * pp + 1] = fmaf(e.w, s[2 * d2 + 1], o16[2 * pp + 1]);
+#endif
                     }
-                }
                 float4 *dst = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4)
@@ -766,13 +802,12 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
 #undef OPF
 #undef OPE
 #undef EFL
-#undef SRD
-#undef ACF
 #undef ACE
 #undef CRD
 #undef CEM
 #undef RWF
-#undef RWE
+#undef LFL
+#undef LEM
     wptc::fence_before_sync();
     __syncthreads();
     wptc::fence_after_sync();

@@ -1,0 +1,61 @@
+"""Build variants of libwpb200.so that differ only in chain_lb build-time switches
+(wp_lb.cuh LB_* macros), for A/B timing on the GPU box:
+
+    python tools/lb_variants.py build NAME=-DLB_EG=2,-DLB_FFMA2=0 ...
+    python tools/lb_variants.py run cfg3          # on the GPU: every built variant, tools/trace_lb.py timing
+
+Variants land in tools/variants/<NAME>/libwpb200.so (git-ignored, travels with gpurun)."""
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "tools", "variants")
+
+
+def build(specs):
+    from paper_2504_08624_b200 import _build as b
+
+    b.build_native()
+    objs = sorted(glob.glob(os.path.join(b.OBJ_DIR, "*.o")))
+    for spec in specs:
+        name, _, flags = spec.partition("=")
+        flags = [f for f in flags.split(",") if f]
+        out = os.path.join(VDIR, name)
+        os.makedirs(out, exist_ok=True)
+        obj = os.path.join(out, "wp_lb.o")
+        cmd = [b.NVCC, *b.ARCH, *b.FLAGS, *flags, "-c", os.path.join(b.CSRC, "wp_lb.cu"), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise SystemExit(r.stderr)
+        spills = [l for l in r.stderr.splitlines() if "chain_lb_kernelILi8ELi2" in l]
+        link = [o for o in objs if not o.endswith("wp_lb.o")] + [obj]
+        r = subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", os.path.join(out, "libwpb200.so"), *link, "-lpthread"],
+                           capture_output=True, text=True)
+        if r.returncode:
+            raise SystemExit(r.stderr)
+        with open(os.path.join(out, "flags.txt"), "w") as fh:
+            fh.write(" ".join(flags) + "\n")
+        print("built", name, flags)
+
+
+def run(cfg):
+    names = sorted(os.listdir(VDIR)) if os.path.isdir(VDIR) else []
+    for name in ["default"] + names:
+        env = dict(os.environ)
+        if name != "default":
+            env["WP_LIB"] = os.path.join(VDIR, name, "libwpb200.so")
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "trace_lb.py"), cfg], capture_output=True,
+                           text=True, env=env, timeout=300)
+        lines = [l for l in r.stdout.splitlines() if "ms per pass" in l or "->" in l]
+        print(f"== {name}: " + (open(os.path.join(VDIR, name, "flags.txt")).read().strip() if name != "default" else ""))
+        print("\n".join(lines) if lines else r.stderr[-2000:])
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2:])
+    else:
+        run(sys.argv[2] if len(sys.argv) > 2 else "cfg3")

@@ -1,7 +1,8 @@
 """Per-tile role timeline of chain_lb (diagnostics): python tools/trace_lb.py [cfg3|cfg5] [seconds]
 Events (ns, %globaltimer): 0 converter start, 1 operands ready, 2 MMA start, 3 MMAs issued,
-4 look-back start, 5 look-back done, 6 scan done (aggregate published), 7 epilogue done,
-8 epilogue start, 9 TMEM read (accumulator free), 10 carry received, 11 state term done."""
+4 look-back start, 5 look-back done, 6 scan done (aggregate published, prefixes in the ring),
+7 epilogue done, 8 scan start (MMAs complete), 9 epilogue has the carry, 10 epilogue has the prefixes,
+11 epilogue state s_m ready, 12 scan work done (before the ring wait), 13 first TMEM chunk loaded."""
 import os
 import sys
 
@@ -13,7 +14,7 @@ import bench  # noqa: E402
 import paper_2504_08624_b200 as wp  # noqa: E402
 from paper_2504_08624_b200 import _native, engine  # noqa: E402
 
-EV = 12
+EV = 16
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 cfg = bench.CONFIGS[name]
 C, fs = cfg["C"], cfg["fs"]
@@ -46,12 +47,23 @@ _native.set_trace(0, 0)
 t = tr.cpu().numpy().astype(np.float64).reshape(tiles, EV)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan)
-names = ["conv0", "opfull", "mma0", "mma1", "lb0", "lbdone", "scan1", "epi1", "-", "carry", "s", "-"]
+names = ["conv0", "opfull", "mma0", "mma1", "lb0", "lbdone", "scan1", "epi1", "scan0", "carry", "ring", "s_m",
+         "scanw", "tm0", "-", "-"]
 print("span us: %.1f" % (np.nanmax(t[:, 7]) / 1e3))
-for a, b in [(0, 1), (1, 2), (2, 3), (3, 6), (4, 5), (6, 9), (5, 9), (9, 10), (10, 7), (0, 7)]:
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 8), (8, 12), (12, 6), (6, 10), (4, 5), (6, 9), (5, 9), (9, 11),
+             (11, 13), (13, 7), (2, 7), (0, 7)]:
     d = (t[:, b] - t[:, a]) / 1e3
     print(f"{names[a]:>6} -> {names[b]:<6} median {np.nanmedian(d):7.2f} us  p90 {np.nanpercentile(d, 90):7.2f}")
 G = min(tiles, 148)
+# gaps inside one role between consecutive local tiles of a CTA
+for a, b, nm in [(7, 10, "epilogue: epi1(i) -> ring(i+1)"), (6, 8, "scan: scan1(i) -> scan0(i+1)"),
+                 (1, 0, "conv: opfull(i) -> conv0(i+1)"), (3, 2, "mma: mma1(i) -> mma0(i+1)")]:
+    g = []
+    for bb in range(G):
+        col_a, col_b = t[bb::G, a], t[bb::G, b]
+        g.append(col_b[1:] - col_a[:-1])
+    g = np.concatenate(g) / 1e3
+    print(f"{nm:34s} median {np.nanmedian(g):6.2f} us  p90 {np.nanpercentile(g, 90):6.2f}")
 for ev in range(EV):
     per = []
     for b in range(G):
