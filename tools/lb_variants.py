@@ -2,6 +2,7 @@
 (wp_lb.cuh LB_* macros), for A/B timing on the GPU box:
 
     python tools/lb_variants.py build NAME=-DLB_EG=2,-DLB_FFMA2=0 ...
+    python tools/lb_variants.py build NAME@REV=...    # wp_lb.cu/.cuh (and wp_internal.h) as of git REV
     python tools/lb_variants.py run cfg3          # on the GPU: every built variant, tools/trace_lb.py timing
 
 Variants land in tools/variants/<NAME>/libwpb200.so (git-ignored, travels with gpurun)."""
@@ -22,11 +23,24 @@ def build(specs):
     objs = sorted(glob.glob(os.path.join(b.OBJ_DIR, "*.o")))
     for spec in specs:
         name, _, flags = spec.partition("=")
+        name, _, rev = name.partition("@")
         flags = [f for f in flags.split(",") if f]
         out = os.path.join(VDIR, name)
         os.makedirs(out, exist_ok=True)
         obj = os.path.join(out, "wp_lb.o")
-        cmd = [b.NVCC, *b.ARCH, *b.FLAGS, *flags, "-c", os.path.join(b.CSRC, "wp_lb.cu"), "-o", obj]
+        src = os.path.join(b.CSRC, "wp_lb.cu")
+        if rev:
+            # the chain kernel sources of an older revision, next to the current other headers
+            sdir = os.path.join(out, "csrc")
+            subprocess.run(["cp", "-r", b.CSRC, sdir + "_tmp"], check=True)
+            subprocess.run(["rm", "-rf", sdir], check=True)
+            os.rename(sdir + "_tmp", sdir)
+            for f in ("wp_lb.cu", "wp_lb.cuh", "wp_internal.h"):
+                txt = subprocess.run(["git", "show", f"{rev}:paper_2504_08624_b200/csrc/{f}"], cwd=ROOT,
+                                     capture_output=True, text=True, check=True).stdout
+                open(os.path.join(sdir, f), "w").write(txt)
+            src = os.path.join(sdir, "wp_lb.cu")
+        cmd = [b.NVCC, *b.ARCH, *b.FLAGS, *flags, "-I", b.CSRC, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise SystemExit(r.stderr)
