@@ -525,6 +525,7 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
                       void *ws, unsigned long long *trace, cudaStream_t st) {
     const long long T = (N + wpk::CT_TOUT - 1) / wpk::CT_TOUT;
     const long long tiles = T * C;
+    if (tiles >= (1LL << 31)) return cudaErrorInvalidValue;  // 32-bit tile arithmetic in the kernel
     wpk::LbArgs a{};
     a.x = x;
     a.y = y;

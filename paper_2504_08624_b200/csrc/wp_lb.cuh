@@ -537,8 +537,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
         for (int i = warp == 1 ? 0 : 1; i < ntiles; i += 2) {
             const int sc4 = i % LB_NC;
             const long long tile = first + (long long)i * stride;
-            const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
-            const long long k = (long long)((unsigned long long)tile / (unsigned long long)a.C);
+            const long long c = (long long)((unsigned)tile % (unsigned)a.C);  // tiles < 2^31 (host check)
+            const long long k = (long long)((unsigned)tile / (unsigned)a.C);
             wptc::mbar_wait_sleep<512>(CEM(sc4), (uint32_t)((i / LB_NC) & 1) ^ 1u);  // slot read by the epilogue
             if (lane == 0) LBTR(tile, 4);
             // c_k = sum_{l < j} MT^l agg(k-1-l) + MT^j incl(kb - 1)
@@ -692,8 +692,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
         for (int i = grp; i < ntiles; i += LB_EG) {
             const int sa = i % LB_NA, sl = i % LB_NL, sc4 = i % LB_NC;
             const long long tile = first + (long long)i * stride;
-            const long long c = (long long)((unsigned long long)tile % (unsigned long long)a.C);
-            const long long n0 = (long long)((unsigned long long)tile / (unsigned long long)a.C) * (long long)CT_TOUT;
+            const long long c = (long long)((unsigned)tile % (unsigned)a.C);
+            const long long n0 = (long long)((unsigned)tile / (unsigned)a.C) * (long long)CT_TOUT;
 #if LB_GROUP_WAIT
             if (row == 0) {
                 lbd::bar_wait<128>(LFL(sl), (uint32_t)((i / LB_NL) & 1));

@@ -35,7 +35,7 @@ def build(specs):
             subprocess.run(["cp", "-r", b.CSRC, sdir + "_tmp"], check=True)
             subprocess.run(["rm", "-rf", sdir], check=True)
             os.rename(sdir + "_tmp", sdir)
-            for f in ("wp_lb.cu", "wp_lb.cuh", "wp_internal.h"):
+            for f in ("wp_lb.cu", "wp_lb.cuh", "wp_internal.h", "wp_tc.cuh"):
                 txt = subprocess.run(["git", "show", f"{rev}:paper_2504_08624_b200/csrc/{f}"], cwd=ROOT,
                                      capture_output=True, text=True, check=True).stdout
                 open(os.path.join(sdir, f), "w").write(txt)

@@ -1,6 +1,7 @@
 """Summarise an ncu --set full report into profiles/ (markdown + json entry).
 
 usage: python tools/ncu_summary.py <report.ncu-rep> <config_id> <title> [--launches launches.csv]
+       [--units channel-samples] [--round r2]
 """
 
 import csv
@@ -97,7 +98,8 @@ def main():
         md.extend(l.rstrip() for l in open(launches) if l.strip() and not l.startswith("=="))
         md.append("```")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    path_md = os.path.join(ROOT, "profiles", f"r1_{cfg}.md")
+    rnd = sys.argv[sys.argv.index("--round") + 1] if "--round" in sys.argv else "r2"
+    path_md = os.path.join(ROOT, "profiles", f"{rnd}_{cfg}.md")
     with open(path_md, "w") as fh:
         fh.write("\n".join(md) + "\n")
     js = os.path.join(ROOT, "profiles", "ncu_summary.json")
