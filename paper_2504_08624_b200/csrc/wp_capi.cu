@@ -210,7 +210,7 @@ struct Pass {
     int fir_flags = 0;
     // tensor-core FIR (FIR-only passes)
     bool fir_tc = false;
-    int tc_Tp = 0, tc_K = 0, tc_W = 0;
+    int tc_Tp = 0, tc_K = 0, tc_W = 0, tc_nin = 2;
     float tc_out_scale = 1.f;
     unsigned char *d_Bimg = nullptr;
     // FFT overlap-save (long FIR-only passes)
@@ -599,7 +599,11 @@ int finalize_pass(Pass &p) {
         p.tc_Tp = (p.T - 1 + 7) / 8 * 8;
         p.tc_K = (p.tc_Tp + wpk::TC_N + 15) / 16 * 16;
         p.tc_W = wpk::TC_N * (wpk::TC_M - 1) + p.tc_K;
-        p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
+        // double-buffered fp32 windows up to 129 taps, one window buffer up to 257 taps (the
+        // B image grows with the taps); beyond that FFT overlap-save is the faster path anyway
+        // (profiles/r2_fir_crossover.md: fir_tc 0.19-0.21 ms vs fft_ols 0.31 ms per pass)
+        p.tc_nin = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, 2) <= 227 * 1024 ? 2 : 1;
+        p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, p.tc_nin) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
     }
     // IIR + FIR passes run on the tensor-core chain kernel; IIR-only passes stay
     // on the CUDA-core chunked scan, which measured faster for them (cfg5
@@ -692,14 +696,15 @@ int finalize_pass(Pass &p) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");
         e = cudaMemcpy(p.d_Bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(Bimg)");
-        p.smem = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K);
+        p.smem = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, p.tc_nin);
         const int occ = wp::fir_tc_occupancy(p.smem);
         if (occ <= 0) return fail(WP_ECUDA, "tensor-core FIR kernel cannot be resident");
         p.grid_cap = occ * wp::sm_count();
         p.Lout = wpk::TC_TOUT;
         char buf[256];
-        snprintf(buf, sizeof buf, "fir_tc[pre=%g taps=%d K=%d post=%zu] tcgen05 f16x3 M128xN64 SW128 tile=%d smem=%zu occ=%d",
-                 (double)p.pre, p.T, p.tc_K, p.post.size(), wpk::TC_TOUT, p.smem, occ);
+        snprintf(buf, sizeof buf,
+                 "fir_tc[pre=%g taps=%d K=%d post=%zu] tcgen05 f16x3 M128xN64 SW128 tile=%d smem=%zu occ=%d windows=%d",
+                 (double)p.pre, p.T, p.tc_K, p.post.size(), wpk::TC_TOUT, p.smem, occ, p.tc_nin);
         p.desc = buf;
         return WP_OK;
     }
@@ -1244,6 +1249,7 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.Tp = p.tc_Tp;
             a.K = p.tc_K;
             a.W = p.tc_W;
+            a.nin = p.tc_nin;
             a.Bimg = p.d_Bimg;
             a.out_scale = p.tc_out_scale;
             a.pre_gain = p.pre;

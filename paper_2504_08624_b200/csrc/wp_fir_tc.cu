@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
     const uint32_t inBytes = ((uint32_t)a.W * 4u + 1023u) & ~1023u;
     const uint32_t stgBytes = (128u * kStagePitch + 1023u) & ~1023u;
     const uint32_t bBytes = (uint32_t)((a.K + 63) / 64) * 8192u;  // one split of B
-    unsigned char *inbuf0 = smem, *inbuf1 = smem + inBytes;
-    unsigned char *stg = smem + 2 * inBytes;  // output staging (padded rows)
+    // fp32 windows: double-buffered, or one buffer (a.nin == 1) when the taps' B image
+    // needs the room (T > 129): the converters free it as soon as it is in registers
+    unsigned char *inbuf0 = smem, *inbuf1 = smem + (a.nin > 1 ? inBytes : 0u);
+    unsigned char *stg = smem + (uint32_t)a.nin * inBytes;  // output staging (padded rows)
     unsigned char *op = stg + stgBytes;       // [stage][hi, lo]
     unsigned char *bimg = op + 4 * opBytes;  // [hi, lo]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(bimg + 2 * bBytes);
@@ -143,8 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
         // ================= bulk-copy producer =================
         if (lane == 0) {
             for (int i = 0; i < ntiles; ++i) {
-                const int s = i & 1;
-                const uint32_t par = (uint32_t)((i >> 1) & 1);
+                const int s = a.nin > 1 ? (i & 1) : 0;
+                const uint32_t par = (uint32_t)((a.nin > 1 ? (i >> 1) : i) & 1);
                 wptc::mbar_wait(BAR(IN_EMPTY, s), par ^ 1u);
                 const Geo g = geo(a, first + (long long)i * stride);
                 const uint32_t bytes = (uint32_t)(4 * (g.hi - g.lo));
@@ -193,10 +195,12 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
         for (int i = 0; i < ntiles; ++i) {
             const int s = i & 1;
             const uint32_t par = (uint32_t)((i >> 1) & 1);
+            const int si = a.nin > 1 ? s : 0;  // fp32 window buffer
+            const uint32_t pari = (uint32_t)((a.nin > 1 ? (i >> 1) : i) & 1);
             const Geo g = geo(a, first + (long long)i * stride);
             const float *xr = a.x + g.c * a.ldx;
-            wptc::mbar_wait(BAR(IN_FULL, s), par);
-            const float4 *in4 = reinterpret_cast<const float4 *>(s ? inbuf1 : inbuf0);
+            wptc::mbar_wait(BAR(IN_FULL, si), pari);
+            const float4 *in4 = reinterpret_cast<const float4 *>(si ? inbuf1 : inbuf0);
             float4 v[kMaxQ];
             float m = 0.f;
             const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
             const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
             if (lane == 0) red[cw] = __uint_as_float(mb);
             named_sync(1, kConv);
-            if (ct == 0) mbar_arrive(BAR(IN_EMPTY, s));  // window s is in registers: free it
+            if (ct == 0) mbar_arrive(BAR(IN_EMPTY, si));  // window si is in registers: free it
             float tmax = red[0];
 #pragma unroll
             for (int w = 1; w < 8; ++w) tmax = fmaxf(tmax, red[w]);
@@ -327,12 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
 
 namespace wp {
 
-size_t fir_tc_smem_bytes(int W, int K) {
+size_t fir_tc_smem_bytes(int W, int K, int nin) {
     const size_t opB = ((size_t)W * 2 + 1023) & ~size_t(1023);
     const size_t inB = ((size_t)W * 4 + 1023) & ~size_t(1023);
     const size_t stgB = ((size_t)128 * wpk::kStagePitch + 1023) & ~size_t(1023);
     const size_t bB = (size_t)((K + 63) / 64) * 8192;
-    return 2 * inB + stgB + 4 * opB + 2 * bB + 12 * 8 + 64 + 1024;  // +1 KB alignment slack
+    return (size_t)nin * inB + stgB + 4 * opB + 2 * bB + 12 * 8 + 64 + 1024;  // +1 KB alignment slack
 }
 
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st) {

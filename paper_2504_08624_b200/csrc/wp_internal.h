@@ -23,6 +23,7 @@ struct FirTcArgs {
     long long C, N, ldx, ldy;
     long long total_tiles;
     int Tp, K, W;
+    int nin;                    // fp32 window buffers (2, or 1 for long taps)
     const unsigned char *Bimg;  // [2][K/16][512]
     float out_scale;            // 2^-f of the taps
     float pre_gain;
@@ -81,7 +82,7 @@ cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long lon
                                  const unsigned int *peak_bits, float target, cudaStream_t st);
 
 // tensor-core FIR (wp_fir_tc.cu)
-size_t fir_tc_smem_bytes(int W, int K);
+size_t fir_tc_smem_bytes(int W, int K, int nin);
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
 int fir_tc_occupancy(size_t smem);
 
