@@ -53,9 +53,8 @@
 //                MMAs complete, Kogge-Stone over rows, aggregate -> global
 //                (early, so other SMs' look-backs see it), row prefixes at
 //                zero carry -> shared ring
-//   warps 12-19  epilogue, two groups of four (even / odd local tiles): once
-//                the carry is known s_m = L_m + M^m c, TMEM -> scale + E s_m ->
-//                padded staging -> coalesced stores
+//   warps 12-15  epilogue: once the carry is known s_m = L_m + M^m c, TMEM ->
+//                scale + E s_m -> padded staging -> coalesced stores
 #pragma once
 
 #include <cuda_fp16.h>
@@ -66,32 +65,13 @@
 
 namespace wpk {
 
-// build-time variants (A/B diagnostics, tools/lb_variants.py); the defaults are the product
-#ifndef LB_EG
-#define LB_EG 1          // epilogue groups of four warps (alternate tiles)
-#endif
-#ifndef LB_E_CONST
-#define LB_E_CONST 0     // E pairs from the kernel parameters (constant bank) instead of shared memory
-#endif
-#ifndef LB_M_CONST
-#define LB_M_CONST 1     // M^(2^b), M^(32 w) from the kernel parameters instead of shared memory
-#endif
-#ifndef LB_GROUP_WAIT
-#define LB_GROUP_WAIT 0  // one waiting thread per role + named barrier (else every warp polls)
-#endif
-#ifndef LB_FFMA2
-#define LB_FFMA2 1       // packed fp32x2 FMAs for E s
-#endif
-constexpr int LB_THREADS = 384 + 128 * LB_EG;
+constexpr int LB_THREADS = 512;
 constexpr int LB_CONV = 160;   // converter threads (warps 2..6)
 constexpr int LB_QMAX = 14;    // float4 of the window per converter thread (W <= 8960)
 constexpr int LB_NA = 6;       // TMEM accumulator stages (80 columns each)
 constexpr int LB_NS = 80;      // TMEM columns per stage: main [0, 64), e [64, 80)
 constexpr int LB_NC = 4;       // carry ring (look-back warp -> epilogue)
-#ifndef LB_NLV
-#define LB_NLV 4
-#endif
-constexpr int LB_NL = LB_NLV;  // row-prefix ring (scan -> epilogue)
+constexpr int LB_NL = 4;       // row-prefix ring (scan -> epilogue)
 constexpr int LB_RING = 16;    // tile-scale ring (converters -> scan)
 constexpr int LB_MAX_H = 256;  // FIR halo limit (W <= 8448)
 constexpr int LB_TRACE_EV = 16;
@@ -147,8 +127,8 @@ struct LbLayout {
         const uint32_t rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         tabs = raw + rawBytes;
         ring = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [NL][D][128] row prefixes
-        stg = ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS);  // [LB_EG groups][4 warps][32 rows] staging
-        misc = stg + 4u * LB_EG * 32u * CT_STG_PITCH;
+        stg = ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS);  // [4 warps][32 rows] staging
+        misc = stg + 4u * 32u * CT_STG_PITCH;
         // misc: Tw[2][4][D], cb[NC][D] f32; scl[RING] f32, rsc[NL] f32, red[8] f32, stag[RING] i32
         bars = (misc + 4u * (uint32_t)((8 + LB_NC) * D) + 4u * (2 * LB_RING + LB_NL + 8) + 15u) & ~15u;
         total = bars + 48 * 8 + 16 + 1024;  // + alignment slack (35 barriers + TMEM slot)
@@ -303,16 +283,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     unsigned char *bimg = smem + lay.bimg;
     unsigned char *op = smem + lay.op;
     float *tabs = reinterpret_cast<float *>(smem + lay.tabs);
-#if LB_M_CONST
     const float *Mp = a.Mpw;
     const float *Wt = a.Mpw + 7 * D * DP;
-#else
-    const float *Mp = tabs + lb_off_mp(D);
-    const float *Wt = tabs + lb_off_wt(D);
-#endif
-#if !LB_E_CONST
     const float4 *Ep = reinterpret_cast<const float4 *>(tabs);  // [32][D / 2]: E pairs of two states
-#endif
     const float *Gl = tabs + lb_off_gl(D);
     float *ring = reinterpret_cast<float *>(smem + lay.ring);  // [NL][D][128] row prefixes (zero carry)
     unsigned char *stg = smem + lay.stg;
@@ -444,12 +417,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
             const float *xr = a.x + g.c * a.ldx;
             const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
-#if LB_GROUP_WAIT
-            if (ct == 0) lbd::bar_wait<256>(RWF, (uint32_t)(i & 1));
-            ctd::named_sync(4, LB_CONV);
-#else
             wptc::mbar_wait_sleep<256>(RWF, (uint32_t)(i & 1));
-#endif
             if (ct == 0) LBTR(first + (long long)i * stride, 0);
             float4 v[LB_QMAX];
             float m = 0.f;
@@ -485,20 +453,13 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             if (lane == 0) red[cw] = __uint_as_float(mb);
             ctd::named_sync(1, LB_CONV);
             if (ct == 0 && i + 1 < ntiles) issue_window(i + 1);  // the window is in registers: refill it
-#if LB_GROUP_WAIT
-            if (ct == 0) lbd::bar_wait<256>(OPE(s), par ^ 1u);
-#endif
             float tmax = red[0];
 #pragma unroll
             for (int w = 1; w < LB_CONV / 32; ++w) tmax = fmaxf(tmax, red[w]);
             int ex = 0;
             if (tmax > 0.f) frexpf(tmax, &ex);
             const float sc = ldexpf(1.f, tmax > 0.f ? 14 - ex : 0);
-#if LB_GROUP_WAIT
-            ctd::named_sync(5, LB_CONV);
-#else
             wptc::mbar_wait_sleep<1024>(OPE(s), par ^ 1u);
-#endif
             unsigned char *ohi = op + (2 * s) * lay.opBytes, *olo = ohi + lay.opBytes;
 #pragma unroll
             for (int j = 0; j < LB_QMAX; ++j) {
@@ -598,23 +559,12 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             const int sa = i % LB_NA;
             const long long tile = first + (long long)i * stride;
             const int sl = i % LB_NL;
-#if LB_GROUP_WAIT
-            if (row == 0) {
-                lbd::bar_wait<128>(EFL(sa), (uint32_t)((i / LB_NA) & 1));
-                for (int spins = 0; *reinterpret_cast<volatile int *>(stag + (i % LB_RING)) != i; ++spins) {
-                    __nanosleep(64);
-                    if (spins > (1 << 28)) __trap();
-                }
-            }
-            ctd::named_sync(6, 128);
-#else
             wptc::mbar_wait_sleep<128>(EFL(sa), (uint32_t)((i / LB_NA) & 1));
             for (int spins = 0; *reinterpret_cast<volatile int *>(stag + (i % LB_RING)) != i; ++spins) {
                 __nanosleep(32);
                 if (spins > (1 << 28)) __trap();
             }
             __threadfence_block();
-#endif
             wptc::fence_after_sync();
             if (row == 0) LBTR(tile, 8);
             float ev[16];
@@ -681,29 +631,20 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             if (row == 0) LBTR(tile, 6);
         }
     } else {
-        // ================= epilogue (warps 12-15: even, 16-19: odd local tiles) =================
+        // ================= epilogue (warps 12-15) =================
         // s_m = L_m + M^m c, TMEM + E s_m -> y
-        const int grp = LB_EG > 1 ? (warp - 12) >> 2 : 0;
         const int wq = warp & 3;
         const int row = 32 * wq + lane;
         const uint32_t trow = (uint32_t)(32 * wq) << 16;
-        unsigned char *mystg = stg + (size_t)(4 * grp + wq) * 32 * CT_STG_PITCH;
+        unsigned char *mystg = stg + (size_t)wq * 32 * CT_STG_PITCH;
 #pragma unroll 1
-        for (int i = grp; i < ntiles; i += LB_EG) {
+        for (int i = 0; i < ntiles; ++i) {
             const int sa = i % LB_NA, sl = i % LB_NL, sc4 = i % LB_NC;
             const long long tile = first + (long long)i * stride;
             const long long c = (long long)((unsigned)tile % (unsigned)a.C);
             const long long n0 = (long long)((unsigned)tile / (unsigned)a.C) * (long long)CT_TOUT;
-#if LB_GROUP_WAIT
-            if (row == 0) {
-                lbd::bar_wait<128>(LFL(sl), (uint32_t)((i / LB_NL) & 1));
-                lbd::bar_wait<128>(CRD(sc4), (uint32_t)((i / LB_NC) & 1));
-            }
-            ctd::named_sync(7 + grp, 128);
-#else
             wptc::mbar_wait_sleep<128>(LFL(sl), (uint32_t)((i / LB_NL) & 1));
             wptc::mbar_wait_sleep<128>(CRD(sc4), (uint32_t)((i / LB_NC) & 1));
-#endif
             float s[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) s[d] = ring[(sl * D + d) * CT_ROWS + row];
@@ -745,20 +686,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                 for (int pp = 0; pp < 8; ++pp)
 #pragma unroll
                     for (int d2 = 0; d2 < D / 2; ++d2) {
-#if LB_E_CONST
-                        const float4 e = a.Ep[(8 * ch + pp) * (D / 2) + d2];  // E[p][2 d2 .. +1], E[p + 1][..]
-#else
                         const float4 e = Ep[(8 * ch + pp) * (D / 2) + d2];
-#endif
-#if LB_FFMA2
                         lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.x, e.y, s[2 * d2]);
                         lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.z, e.w, s[2 * d2 + 1]);
-#else
-                        o16[2 * pp] = fmaf(e.x, s[2 * d2], o16[2 * pp]);
-                        o16[2 * pp + 1] = fmaf(e.y, s[2 * d2], o16[2 * pp + 1]);
-                        o16[2 * pp] = fmaf(e.z, s[2 * d2 + 1], o16[2 * pp]);
-                        o16[2 * pp + 1] = fmaf(e.w, s[2 * d2 + 1], o16[2 * pp + 1]);
-#endif
                     }
                 float4 *dst = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
 #pragma unroll
