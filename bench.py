@@ -431,8 +431,6 @@ def main():
     algo_bytes = 8.0 * units  # fp32 read once + write once per channel-sample
     passes = plan.describe_for(max(C, 1), N)
     kernel_names = {"chain_lb": "wpk::chain_lb_kernel", "fir_tc": "wpk::fir_tc_kernel",
-                    "chain_rows+chain_carry+chain_gemm":
-                        "wpk::chain_rows_kernel + wpk::chain_carry_kernel + wpk::chain_gemm_kernel",
                     "fft_ols": "wpk::fft_ols_kernel", "fused": "wpk::fused_chain_kernel"}
     kernels = [kernel_names.get(d.split("[")[0], d.split("[")[0]) for d in passes]
     achieved = algo_bytes / (per_launch_ms / 1e3) / 1e9
@@ -479,7 +477,7 @@ def main():
     if parity is not None:
         line["parity_check"] = parity
     taps = sum(len(getattr(st, "taps", ())) for st in stages)
-    if any(("chain_lb" in k or "fir_tc" in k or "chain_gemm" in k) for k in kernels) and taps:
+    if any(("chain_lb" in k or "fir_tc" in k) for k in kernels) and taps:
         # algorithmic FIR flops = 2 T per channel-sample, against
         # the dense fp16 tensor peak; the fp16 x3 split runs 3x those MMAs
         tflops = 2.0 * taps * units / (per_launch_ms / 1e3) / 1e12

@@ -91,7 +91,7 @@ int wp_plan_launches(const wp_plan *plan);
 /* Human-readable description of pass i (kernel kind, sections, taps, precision). */
 const char *wp_plan_describe(const wp_plan *plan, int32_t pass);
 /* The same for one call shape: IIR-only passes run the fused scan kernel for
- * small calls and the three-kernel tensor-core chain for large ones. */
+ * small calls and the single-pass tensor-core chain (chain_lb) for large ones. */
 int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames);
 const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t channels, int64_t frames);
 

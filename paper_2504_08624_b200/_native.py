@@ -212,7 +212,7 @@ class Plan:
 
     def describe_for(self, channels: int, frames: int):
         """Kernels each pass launches for this call shape (IIR-only passes
-        switch from the fused scan to the three-kernel chain on large calls)."""
+        switch from the fused scan to chain_lb on large calls)."""
         return [self._lib.wp_plan_describe_for(self.handle, i, channels, frames).decode()
                 for i in range(self.num_passes)]
 

@@ -217,25 +217,6 @@ struct Pass {
     bool fft = false;
     int fft_Tpad = 0;
     float2 *d_H = nullptr, *d_tw = nullptr;
-    // tensor-core chain (IIR [+ FIR] passes)
-    bool chain_tc = false;
-    int ct_H = 0, ct_K = 0, ct_W = 0;
-    float ct_out_scale = 1.f;
-    std::vector<double> ct_E;  // [64][D]
-    unsigned char *d_Bk = nullptr;  // int8 digit planes of the chunk-state weights
-    double ct_kscale[8] = {0};
-    // decoupled tensor-core chain (rows -> carry -> gemm kernels)
-    bool chain3 = false;
-    int c3_nop = 2;                   // fp16 operand stages of chain_gemm
-    unsigned char *d_Eimg = nullptr;  // tf32 parts of the state-term matrix E
-    double c3_st_scale = 1.0;
-    // IIR-only passes keep the fused kernel for small calls and switch to the
-    // three-kernel chain from c3_min_tiles tiles on (both built at plan time)
-    bool c3_large = false;
-    long long c3_min_tiles = 0;
-    size_t c3_smem = 0;
-    int c3_grid_cap = 0;
-    std::string c3_desc;
     // single-pass tensor-core chain with look-back (wp_lb.cuh): IIR [+ FIR] passes;
     // IIR-only passes of <= 4 sections keep the fused kernel for small calls
     bool lb = false, lb_large = false;
@@ -281,216 +262,17 @@ bool fir_tc_enabled() {
     return !(v && std::string(v) == "cuda");
 }
 
-bool chain_tc_enabled() {
+// WP_CHAIN_IMPL=cuda: IIR passes on the CUDA-core chunked scan only; =lb: chain_lb
+// for every IIR-only call, however small (A/B diagnostics and tests)
+bool lb_enabled() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
     return !(v && std::string(v) == "cuda");
 }
-
-bool chain_tc_forced() {
+bool lb_forced() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
-    return v && (std::string(v) == "tc" || std::string(v) == "tc1");
+    return v && std::string(v) == "lb";
 }
 
-// WP_CHAIN_IMPL=tc1 selects the single-kernel look-back chain (wp_chain_tc.cuh)
-// instead of the decoupled three-kernel chain (wp_chain3.cuh).
-bool chain_single_kernel() {
-    const char *v = std::getenv("WP_CHAIN_IMPL");
-    return v && std::string(v) == "tc1";
-}
-
-// default: single-pass look-back chain; WP_CHAIN_IMPL=c3 / cuda / tc / tc1 select the
-// round-1 kernels for A/B comparisons
-bool lb_enabled() {
-    const char *v = std::getenv("WP_CHAIN_IMPL");
-    return !(v && (std::string(v) == "c3" || std::string(v) == "cuda" || std::string(v) == "tc" ||
-                   std::string(v) == "tc1"));
-}
-
-float tf32_round(double v) {
-    float f = (float)v;
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    u = (u + 0x1000u) & 0xFFFFE000u;
-    std::memcpy(&f, &u, 4);
-    return f;
-}
-
-// Build the tensor-core chain tables of pass p: combined response g (Toeplitz
-// B image, fp16 hi/lo), state-term matrix E, chunk-scan tables (M = A^64).
-int build_chain_tc(Pass &p, int H, int K, int W, bool f64, size_t smem) {
-    const int S = p.S, D = 2 * S;
-    Mat A;
-    std::vector<double> B, C;
-    double d = 0;
-    cascade_ss(p.sos, S, A, B, C, d);
-    double gain = (double)p.pre;
-    for (float g : p.post) gain *= (double)g;
-    std::vector<double> f = p.T > 0 ? p.taps : std::vector<double>{1.0};
-    const int T = (int)f.size();
-    // CA[t] = C A^t, t < H + 64
-    std::vector<double> CA((size_t)(H + 64) * D);
-    std::vector<double> row = C, nrow(D);
-    for (int t = 0; t < H + 64; ++t) {
-        for (int i = 0; i < D; ++i) CA[(size_t)t * D + i] = row[i];
-        for (int j = 0; j < D; ++j) {
-            long double acc = 0;
-            for (int i = 0; i < D; ++i) acc += (long double)row[i] * A[i * D + j];
-            nrow[j] = (double)acc;
-        }
-        row = nrow;
-    }
-    // impulse response h[t] = d (t = 0), C A^(t-1) B
-    std::vector<double> h(K);
-    h[0] = d;
-    for (int t = 1; t < K; ++t) {
-        long double acc = 0;
-        for (int i = 0; i < D; ++i) acc += (long double)CA[(size_t)(t - 1) * D + i] * B[i];
-        h[t] = (double)acc;
-    }
-    std::vector<double> g(K, 0.0);
-    for (int t = 0; t < K; ++t) {
-        long double acc = 0;
-        for (int k = 0; k < T && k <= t; ++k) acc += (long double)f[k] * h[t - k];
-        g[t] = (double)(acc * gain);
-    }
-    p.ct_E.assign(64 * D, 0.0);
-    for (int q = 0; q < 64; ++q)
-        for (int i = 0; i < D; ++i) {
-            long double acc = 0;
-            for (int k = 0; k < T; ++k) acc += (long double)f[k] * CA[(size_t)(H + q - k) * D + i];
-            p.ct_E[q * D + i] = (double)(acc * gain);
-        }
-    // B image: B[q, k] = g[q + H - k], K-major SW128, fp16 hi / lo (x 2^11)
-    double gmax = 0;
-    for (double v : g) gmax = std::max(gmax, std::fabs(v));
-    int ex = 0;
-    if (gmax > 0) std::frexp(gmax, &ex);
-    const int fB = gmax > 0 ? 14 - ex : 0;
-    p.ct_out_scale = (float)std::ldexp(1.0, -fB);
-    const int atoms = (K + 63) / 64;
-    const size_t split = (size_t)atoms * 8192 / sizeof(__half);
-    std::vector<__half> img(2 * split, __float2half_rn(0.f));
-    for (int q = 0; q < 64; ++q)
-        for (int k = 0; k < K; ++k) {
-            const int t = q + H - k;
-            const float val = (t >= 0 && t < K) ? (float)std::ldexp(g[t], fB) : 0.f;
-            const __half hi = __float2half_rn(val);
-            const __half lo = __float2half_rn(val - __half2float(hi));  // unscaled: one accumulator
-            if (chain_single_kernel()) {
-                // [part][atom][64 rows][128 B]
-                const uint32_t logical = (uint32_t)(k / 64) * 8192u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
-                const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
-                img[phys / 2] = hi;
-                img[split + phys / 2] = lo;
-            } else {
-                // [atom][hi rows 0..63 | lo rows 64..127][128 B]: one N = 128 operand per K atom
-                const uint32_t logical = (uint32_t)(k / 64) * 16384u + (uint32_t)q * 128u + (uint32_t)(k % 64) * 2u;
-                const uint32_t phys = logical ^ (((logical >> 7) & 7u) << 4);
-                img[phys / 2] = hi;
-                img[(phys + 8192u) / 2] = lo;
-            }
-        }
-    cudaError_t e = cudaMalloc(&p.d_Bimg, img.size() * sizeof(__half));
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(Bimg)");
-    e = cudaMemcpy(p.d_Bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(Bimg)");
-    // chunk-scan tables: K[n] = A^(63-n) B, M = A^64, tiles of 128 chunks
-    build_tables(p.tables, p.sos, S, 0);
-    // exact e-GEMM operand: K[n][d] as 31-bit fixed point per state d, 4 int8
-    // digits (top digit signed), K-major no-swizzle rows of 64 bytes
-    {
-        std::vector<unsigned char> bk((size_t)wpk::CT_KD * 1024, 0);
-        for (int d = 0; d < D; ++d) {
-            double kmax = 0;
-            for (int n = 0; n < 64; ++n) kmax = std::max(kmax, std::fabs(p.tables.K[n * D + d]));
-            int kex = 0;
-            if (kmax > 0) std::frexp(kmax, &kex);
-            const int kappa = kmax > 0 ? 30 - kex : 0;
-            p.ct_kscale[d] = std::ldexp(1.0, -kappa);
-            for (int n = 0; n < 64; ++n) {
-                const long long q = std::llround(std::ldexp(p.tables.K[n * D + d], kappa));
-                const uint32_t u = (uint32_t)(int32_t)q;
-                for (int b = 0; b < wpk::CT_KD; ++b)
-                    bk[(size_t)b * 1024 + wpk::ctd::dg_off(d, n)] = (unsigned char)((u >> (8 * b)) & 255u);
-            }
-        }
-        cudaError_t e2 = cudaMalloc(&p.d_Bk, bk.size());
-        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaMalloc(Bk)");
-        e2 = cudaMemcpy(p.d_Bk, bk.data(), bk.size(), cudaMemcpyHostToDevice);
-        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaMemcpy(Bk)");
-    }
-    const size_t es = f64 ? sizeof(double) : sizeof(float);
-    std::vector<unsigned char> gbuf(es * D * D * 33), tbuf(es * 33 * D * D);
-    for (size_t i = 0; i < p.tables.G.size(); ++i) {
-        if (f64)
-            reinterpret_cast<double *>(gbuf.data())[i] = p.tables.G[i];
-        else
-            reinterpret_cast<float *>(gbuf.data())[i] = (float)p.tables.G[i];
-    }
-    for (size_t i = 0; i < p.tables.TP.size(); ++i) {
-        if (f64)
-            reinterpret_cast<double *>(tbuf.data())[i] = p.tables.TP[i];
-        else
-            reinterpret_cast<float *>(tbuf.data())[i] = (float)p.tables.TP[i];
-    }
-    e = cudaMalloc(&p.d_G, gbuf.size());
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(G)");
-    e = cudaMalloc(&p.d_TP, tbuf.size());
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(TP)");
-    e = cudaMemcpy(p.d_G, gbuf.data(), gbuf.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(G)");
-    e = cudaMemcpy(p.d_TP, tbuf.data(), tbuf.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(TP)");
-    p.chain_tc = true;
-    if (!chain_single_kernel()) {
-        // state-term operand of chain_gemm: E[p][d] x 2^fB in three tf32 parts,
-        // no-swizzle K-major rows of 8 states (32 B), zero for d >= D
-        std::vector<float> eimg(3 * 512, 0.f);
-        for (int q = 0; q < 64; ++q)
-            for (int i = 0; i < D; ++i) {
-                const double v = p.ct_E[q * D + i];
-                const float t1 = tf32_round(v);
-                const double r1 = v - (double)t1;
-                const float t2 = tf32_round(r1);
-                const float t3 = tf32_round(r1 - (double)t2);
-                const uint32_t o = wpk::c3d::off32(q, i) / 4;
-                eimg[o] = t1;
-                eimg[512 + o] = t2;
-                eimg[1024 + o] = t3;
-            }
-        cudaError_t e3 = cudaMalloc(&p.d_Eimg, eimg.size() * sizeof(float));
-        if (e3 != cudaSuccess) return cuda_fail(e3, "cudaMalloc(Eimg)");
-        e3 = cudaMemcpy(p.d_Eimg, eimg.data(), eimg.size() * sizeof(float), cudaMemcpyHostToDevice);
-        if (e3 != cudaSuccess) return cuda_fail(e3, "cudaMemcpy(Eimg)");
-        p.c3_st_scale = std::ldexp(1.0, fB);
-        p.chain3 = true;
-        p.chain_tc = false;
-        // a third operand stage when it fits (K = 64 IIR-only passes; not cfg3's K = 176)
-        p.c3_nop = wp::chain3_smem_bytes(W, K, S, f64, 3) <= 227 * 1024 ? 3 : 2;
-        smem = wp::chain3_smem_bytes(W, K, S, f64, p.c3_nop);
-    }
-    p.f64 = f64;
-    p.ct_H = H;
-    p.ct_K = K;
-    p.ct_W = W;
-    p.smem = smem;
-    p.grid_cap = wp::sm_count();
-    p.Lout = wpk::CT_TOUT;
-    char buf[256];
-    if (p.chain3)
-        snprintf(buf, sizeof buf,
-                 "chain_rows+chain_carry+chain_gemm[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3+tf32x6 M128xN64 "
-                 "K=%d halo=%d tile=%d stages=%d smem=%zu",
-                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, p.c3_nop, smem);
-    else
-        snprintf(buf, sizeof buf,
-                 "chain_tc[pre=%g iir=%d(%s) fir=%d post=%zu] tcgen05 f16x3 M128xN64 K=%d halo=%d tile=%d smem=%zu",
-                 (double)p.pre, p.S, f64 ? "f64" : "f32", p.T, p.post.size(), K, H, wpk::CT_TOUT, smem);
-    p.desc = buf;
-    return WP_OK;
-}
-
-// Iterative radix-2 FFT in float64 (plan time only), in place, forward.
 void host_fft(std::vector<std::complex<double>> &a) {
     const size_t n = a.size();
     for (size_t i = 1, j = 0; i < n; ++i) {
@@ -554,16 +336,6 @@ int build_fft(Pass &p) {
     return WP_OK;
 }
 
-void free_pass_c3(Pass &q) {
-    if (q.d_Bimg) cudaFree(q.d_Bimg);
-    if (q.d_Eimg) cudaFree(q.d_Eimg);
-    if (q.d_G) cudaFree(q.d_G);
-    if (q.d_TP) cudaFree(q.d_TP);
-    if (q.d_Bk) cudaFree(q.d_Bk);
-    q.d_Bimg = q.d_Eimg = q.d_Bk = nullptr;
-    q.d_G = q.d_TP = nullptr;
-}
-
 int finalize_pass(Pass &p) {
     if (p.kind != Pass::FUSED) {
         char buf[128];
@@ -586,7 +358,7 @@ int finalize_pass(Pass &p) {
         // IIR-only: small calls keep the fused chunked scan (one launch, exact
         // per-chunk recurrence for the known-answer cases)
         p.lb_large = true;
-        p.lb_min_tiles = 2LL * wp::sm_count();
+        p.lb_min_tiles = lb_forced() ? 0 : 2LL * wp::sm_count();
         if (p.T == 1) {
             // a 1-tap FIR is a gain: the fused kernel takes it as a post gain
             p.post.push_back((float)p.taps[0]);
@@ -604,65 +376,6 @@ int finalize_pass(Pass &p) {
         // (profiles/r2_fir_crossover.md: fir_tc 0.19-0.21 ms vs fft_ols 0.31 ms per pass)
         p.tc_nin = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, 2) <= 227 * 1024 ? 2 : 1;
         p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, p.tc_nin) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
-    }
-    // IIR + FIR passes run on the tensor-core chain kernel; IIR-only passes stay
-    // on the CUDA-core chunked scan, which measured faster for them (cfg5
-    // slice 295 vs 254 G ch-s/s, cfg3's IIR part 0.97 vs 1.25 ms;
-    // tools/iir_probe.py). WP_CHAIN_IMPL=tc forces the tensor-core kernel.
-    if (p.S > 0 && p.T == 0 && chain_tc_enabled() && !chain_tc_forced() && !p.lb_large) {
-        // large IIR-only calls: the three-kernel chain beats the fused scan
-        // (cfg5: 42.5 vs 47.7 ms); small ones keep the fused kernel (fewer
-        // launches; exact per-chunk recurrence for the known-answer cases)
-        double rmax = 0;
-        for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
-        const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
-        const int W = wpk::CT_TOUT, K = 64;
-        const size_t smem = wp::chain3_smem_bytes(W, K, p.S, f64, 2);
-        if (smem <= 227 * 1024) {
-            Pass q = p;
-            int rc = build_chain_tc(q, 0, K, W, f64, smem);
-            if (rc != WP_OK) {
-                free_pass_c3(q);
-                return rc;
-            }
-            p.d_Bimg = q.d_Bimg;
-            p.d_Eimg = q.d_Eimg;
-            p.ct_H = q.ct_H;
-            p.ct_K = q.ct_K;
-            p.ct_W = q.ct_W;
-            p.ct_out_scale = q.ct_out_scale;
-            p.c3_st_scale = q.c3_st_scale;
-            p.ct_E = q.ct_E;
-            p.c3_smem = q.smem;
-            p.c3_nop = q.c3_nop;
-            p.c3_grid_cap = q.grid_cap;
-            p.c3_desc = q.desc;
-            p.c3_large = true;
-            p.c3_min_tiles = 8LL * wp::sm_count();
-            // the fused build below uploads the same scan tables (H = 0)
-            if (q.d_G) cudaFree(q.d_G);
-            if (q.d_TP) cudaFree(q.d_TP);
-            if (q.d_Bk) cudaFree(q.d_Bk);
-        }
-    }
-    if (p.S > 0 && !p.lb_large && chain_tc_enabled() && (p.T > 1 || chain_tc_forced())) {
-        const int T = p.T > 0 ? p.T : 1;
-        const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
-        const int K = H + 64;
-        const int W = wpk::CT_TOUT + H;
-        if (H <= wpk::CT_MAX_H) {
-        double rmax = 0;
-        for (int s = 0; s < p.S; ++s) rmax = std::max(rmax, section_radius(&p.sos[5 * s]));
-        const bool f64 = (p.prec_flag & WP_IIR_PREC_F64) ? true : (p.prec_flag & WP_IIR_PREC_F32) ? false : rmax > kF64Radius;
-        const size_t smem = chain_single_kernel() ? wp::chain_tc_smem_bytes(W, K, p.S, f64)
-                                                  : wp::chain3_smem_bytes(W, K, p.S, f64, 2);
-        const int qcap = chain_single_kernel() ? wpk::CT_QMAX * wpk::CT_CONV : wpk::C3_QMAX * wpk::C3_CONV;
-        if (W / 4 <= qcap && smem <= 227 * 1024) {
-            int rc = build_chain_tc(p, H, K, W, f64, smem);
-            if (rc != WP_OK) return rc;
-            return WP_OK;
-        }
-        }
     }
     if (p.S == 0 && p.T > 1 && !(p.fir_flags & WP_FIR_DIRECT) && ((p.fir_flags & WP_FIR_FFT) || !p.fir_tc)) {
         p.fir_tc = false;
@@ -764,7 +477,6 @@ int finalize_pass(Pass &p) {
     snprintf(buf, sizeof buf, "fused[pre=%g iir=%d%s fir=%d post=%zu] tile=%d halo=%d smem=%zu occ=%d", (double)p.pre, p.S,
              p.S ? (p.f64 ? "(f64)" : "(f32)") : "", p.T, p.post.size(), p.Lout, p.H, p.smem, occ);
     p.desc = buf;
-    if (p.c3_large) p.desc += " ; from " + std::to_string(p.c3_min_tiles) + " tiles: " + p.c3_desc;
     if (p.lb_large) p.desc += " ; from " + std::to_string(p.lb_min_tiles) + " tiles: " + p.lbp.desc;
     return WP_OK;
 }
@@ -773,10 +485,6 @@ void free_pass(Pass &p) {
     wp::lb_free(p.lbp);
     if (p.d_Bimg) cudaFree(p.d_Bimg);
     p.d_Bimg = nullptr;
-    if (p.d_Bk) cudaFree(p.d_Bk);
-    p.d_Bk = nullptr;
-    if (p.d_Eimg) cudaFree(p.d_Eimg);
-    p.d_Eimg = nullptr;
     if (p.d_H) cudaFree(p.d_H);
     if (p.d_tw) cudaFree(p.d_tw);
     p.d_H = p.d_tw = nullptr;
@@ -790,10 +498,7 @@ void free_pass(Pass &p) {
 size_t rec_bytes(const Pass &p) {
     if (p.kind != Pass::FUSED || p.S == 0) return 0;
     const size_t es = p.f64 ? 8 : 4;
-    const size_t c3b = (size_t)(2 * p.S) * es * (wpk::CT_ROWS + 5);  // row prefixes, tile aggregate, 4 carries
-    if (p.chain3) return c3b;
-    const size_t fb = (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;
-    return p.c3_large ? std::max(fb, c3b) : fb;
+    return (16 + 2 * (size_t)(2 * p.S) * es + 15) / 16 * 16;  // fused kernel's look-back record per tile
 }
 
 long long tiles_per_channel(const Pass &p, long long N) { return (N + p.Lout - 1) / p.Lout; }
@@ -1030,19 +735,16 @@ int wp_plan_num_passes(const wp_plan *plan) { return plan ? (int)plan->passes.si
 int wp_plan_launches(const wp_plan *plan) {
     if (!plan) return 0;
     int n = 0;
-    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : p.lb ? 1 : p.chain3 ? 3 : 1;
+    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : 1;
     return n;
 }
 
-static bool uses_c3(const Pass &p, int64_t C, int64_t N) {
-    return p.chain3 || (p.c3_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.c3_min_tiles);
-}
 
 int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames) {
     if (!plan) return 0;
     int n = 0;
     for (const Pass &p : plan->passes)
-        n += p.kind != Pass::FUSED ? 2 : uses_lb(p, channels, frames) ? 1 : uses_c3(p, channels, frames) ? 3 : 1;
+        n += p.kind != Pass::FUSED ? 2 : 1;
     return n;
 }
 
@@ -1051,7 +753,6 @@ const char *wp_plan_describe_for(const wp_plan *plan, int32_t pass, int64_t chan
     const Pass &p = plan->passes[pass];
     if (p.lb) return p.desc.c_str();
     if (p.lb_large) return uses_lb(p, channels, frames) ? p.lbp.desc.c_str() : p.desc.c_str();
-    if (p.c3_large) return uses_c3(p, channels, frames) ? p.c3_desc.c_str() : p.desc.c_str();
     return p.desc.c_str();
 }
 
@@ -1142,101 +843,6 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             const int grid = (int)std::min<long long>(a.total, p.grid_cap);
             e = wp::launch_fft_ols(a, grid, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
-        } else if (p.chain3 || (p.c3_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.c3_min_tiles)) {
-            wp::Chain3Launch L;
-            const long long T = (N + wpk::CT_TOUT - 1) / wpk::CT_TOUT;
-            const long long tiles = T * C;
-            if (tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
-            const int D = 2 * p.S;
-            const size_t es = p.f64 ? 8 : 4;
-            unsigned char *rows = ws + rec_off;
-            unsigned char *aggs = rows + (size_t)tiles * wpk::CT_ROWS * D * es;
-            unsigned char *carry = aggs + (size_t)tiles * D * es;
-            const int vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
-            const int vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-            L.rows = wpk::C3RowsArgs{in, C, N, ld_in, tiles, p.ct_H, vec_x, p.d_G, rows, aggs};
-            const int B = (int)((T + wpk::C3_CARRY_THREADS - 1) / wpk::C3_CARRY_THREADS);
-            L.carry = wpk::C3CarryArgs{C, T, B, nullptr, aggs, carry};
-            if (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV + (size_t)C * 8)
-                L.carry.trace = g_trace + (size_t)tiles * wpk::C3_TRACE_EV;
-            {
-                // tile transfer M^128; thread-block and warp powers
-                const Mat &MT = p.tables.MT;
-                const Mat MB = matpow(MT, B, D);
-                L.carry_mats.assign((size_t)7 * D * D, 0.0);
-                std::copy(MT.begin(), MT.end(), L.carry_mats.begin());
-                Mat q = MB;
-                for (int i = 0; i < 5; ++i) {
-                    std::copy(q.begin(), q.end(), L.carry_mats.begin() + (size_t)(1 + i) * D * D);
-                    q = matmul(q, q, D);
-                }
-                const Mat R = matpow(MB, 32, D);
-                std::copy(R.begin(), R.end(), L.carry_mats.begin() + (size_t)6 * D * D);
-            }
-            wpk::C3GemmArgs &g = L.gemm;
-            g = wpk::C3GemmArgs{};
-            g.x = in;
-            g.y = out;
-            g.C = C;
-            g.N = N;
-            g.ldx = ld_in;
-            g.ldy = ld_out;
-            g.total_tiles = tiles;
-            g.H = p.ct_H;
-            g.K = p.ct_K;
-            g.W = p.ct_W;
-            g.Bimg = p.d_Bimg;
-            g.Eimg = p.d_Eimg;
-            g.out_scale = p.ct_out_scale;
-            g.st_scale = p.c3_st_scale;
-            g.G = p.d_G;
-            g.rows = rows;
-            g.carry = carry;
-            g.vec_x = vec_x;
-            g.vec_y = vec_y;
-            {
-                const char *dv = std::getenv("WP_CT_DBG");
-                g.dbg = dv ? std::atoi(dv) : 0;
-            }
-            g.trace = (g_trace && g_trace_entries >= (size_t)tiles * wpk::C3_TRACE_EV) ? g_trace : nullptr;
-            L.gemm_grid = (int)std::min<long long>(tiles, p.chain3 ? p.grid_cap : p.c3_grid_cap);
-            L.smem = p.chain3 ? p.smem : p.c3_smem;
-            L.nop = p.c3_nop;
-            e = wp::launch_chain3(p.f64, p.S, L, p.tables, stream);
-            if (e != cudaSuccess) return cuda_fail(e, "chain3 launch");
-        } else if (p.chain_tc) {
-            wpk::ChainTcArgs a{};
-            a.x = in;
-            a.y = out;
-            a.C = C;
-            a.N = N;
-            a.ldx = ld_in;
-            a.ldy = ld_out;
-            a.total_tiles = ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C;
-            if (a.total_tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
-            a.H = p.ct_H;
-            a.K = p.ct_K;
-            a.W = p.ct_W;
-            a.Bimg = p.d_Bimg;
-            a.Bk = p.d_Bk;
-            for (int d = 0; d < 8; ++d) a.kscale[d] = p.ct_kscale[d];
-            a.out_scale = p.ct_out_scale;
-            a.G = p.d_G;
-            a.TP = p.d_TP;
-            a.recs = ws + rec_off;
-            a.epoch = 1;
-            e = cudaMemsetAsync(a.recs, 0, rec_bytes(p) * (size_t)(((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C), stream);
-            if (e != cudaSuccess) return cuda_fail(e, "memset(records)");
-            a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
-            a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-            {
-                const char *dv = std::getenv("WP_CT_DBG");
-                a.dbg = dv ? std::atoi(dv) : 0;
-            }
-            a.trace = (g_trace && g_trace_entries >= (size_t)a.total_tiles * wpk::CT_TRACE_EV) ? g_trace : nullptr;
-            const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
-            e = wp::launch_chain_tc(p.f64, p.S, a, p.tables, p.ct_E, grid, p.smem, stream);
-            if (e != cudaSuccess) return cuda_fail(e, "chain_tc launch");
         } else if (p.fir_tc) {
             wpk::FirTcArgs a{};
             a.x = in;

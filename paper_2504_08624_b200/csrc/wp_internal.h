@@ -8,8 +8,6 @@
 #include <string>
 #include <vector>
 
-#include "wp_chain3.cuh"
-#include "wp_chain_tc.cuh"
 #include "wp_fused.cuh"
 
 namespace wpk {
@@ -85,24 +83,6 @@ cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long lon
 size_t fir_tc_smem_bytes(int W, int K, int nin);
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
 int fir_tc_occupancy(size_t smem);
-
-// tensor-core chain (wp_chain_tc.cu)
-size_t chain_tc_smem_bytes(int W, int K, int S, bool f64);
-cudaError_t launch_chain_tc(bool f64, int S, const wpk::ChainTcArgs &a, const HostTables &t,
-                            const std::vector<double> &E, int grid, size_t smem, cudaStream_t st);
-
-// decoupled tensor-core chain (wp_chain3.cu): chain_rows -> chain_carry -> chain_gemm
-struct Chain3Launch {
-    wpk::C3RowsArgs rows;
-    wpk::C3CarryArgs carry;
-    wpk::C3GemmArgs gemm;
-    std::vector<double> carry_mats;  // [7][D][D]: MT = M^32, MT^(B 2^i) i < 5, MT^(32 B)
-    int gemm_grid = 1;
-    size_t smem = 0;
-    int nop = 2;  // fp16 operand stages of chain_gemm (3 when they fit next to the rest)
-};
-size_t chain3_smem_bytes(int W, int K, int S, bool f64, int nop);
-cudaError_t launch_chain3(bool f64, int S, const Chain3Launch &L, const HostTables &t, cudaStream_t st);
 
 // single-pass tensor-core chain with look-back (wp_lb.cu / wp_lb.cuh)
 struct LbPlan {

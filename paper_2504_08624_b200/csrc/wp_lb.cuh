@@ -61,7 +61,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "wp_chain3.cuh"
+#include "wp_common.cuh"
 
 namespace wpk {
 

@@ -429,7 +429,7 @@ def test_many_channels_lp8_subset_parity():
         assert oracle.parity_error(y[c:c + 1], ref) <= IIR_TOL, c
 
 
-# ---- chain passes: single-pass chain_lb (default) and the round-1 three-kernel chain (WP_CHAIN_IMPL=tc)
+# ---- chain passes: single-pass chain_lb
 
 
 @pytest.mark.gpu
@@ -461,16 +461,16 @@ def test_chain_pass_matrix_vs_oracle(order, precision, taps):
 @pytest.mark.gpu
 @pytest.mark.parametrize("order", [1, 4, 8])
 def test_chain_pass_iir_only_forced(order, monkeypatch):
-    """IIR-only passes through the three-kernel chain (H = 0, K = 64) when it
-    is forced; the default planner keeps them on the fused kernel."""
+    """IIR-only passes through chain_lb (H = 0, K = 64) at a size where the
+    default planner keeps the fused kernel (WP_CHAIN_IMPL=lb forces it)."""
     import torch
 
     fs = 48000
     filt = wp.design_butterworth("lp", order, 2000, fs)
     bound = wp.Chain([filt]).bind(fs).stages
-    monkeypatch.setenv("WP_CHAIN_IMPL", "tc")
+    monkeypatch.setenv("WP_CHAIN_IMPL", "lb")
     plan = _native.Plan(tuple(wp.engine._entry(s) for s in bound))  # uncached: the env var applies
-    assert "chain_gemm" in plan.describe()[0]
+    assert "chain_lb" in plan.describe_for(5, 60001)[0]
     rng = np.random.default_rng(order)
     C, N = 5, 60001
     x = rng.standard_normal((C, N)).astype(np.float32)

@@ -2,7 +2,7 @@
 # the default headline run and the reference arm -> gpurun_out/bench_r2/
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/bench_r2
-timeout 120 python tools/c3_prof.py cfg1 2 > /dev/null || { echo "smoke hung"; exit 1; }
+timeout 120 python tools/run_config.py cfg1 2 > /dev/null || { echo "smoke hung"; exit 1; }
 timeout 600 python bench.py > gpurun_out/bench_r2/bench_default.json 2> gpurun_out/bench_r2/bench_default.err; tail -1 gpurun_out/bench_r2/bench_default.json | cut -c1-300
 timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_r2/bench_reference.json 2> gpurun_out/bench_r2/bench_reference.err; tail -1 gpurun_out/bench_r2/bench_reference.json | cut -c1-300
 for c in cfg1 cfg2 cfg4 cfg5; do

@@ -1,5 +1,5 @@
 """Run one config's plan a few times (for ncu launch lists / captures).
-python tools/c3_prof.py cfg3 [reps]"""
+python tools/run_config.py cfg3 [reps]"""
 import sys
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import torch
