@@ -216,7 +216,8 @@ struct Pass {
     // FFT overlap-save (long FIR-only passes)
     bool fft = false;
     int fft_Tpad = 0;
-    float2 *d_H = nullptr, *d_tw = nullptr;
+    int fft_segs = 1;        // > 1: taps split into segments of kFftSegTaps, one launch each (accumulating)
+    float2 *d_H = nullptr, *d_tw = nullptr;  // d_H: [segs][M]
     // single-pass tensor-core chain with look-back (wp_lb.cuh): IIR [+ FIR] passes;
     // IIR-only passes of <= 4 sections keep the fused kernel for small calls
     bool lb = false, lb_large = false;
@@ -293,33 +294,47 @@ void host_fft(std::vector<std::complex<double>> &a) {
     }
 }
 
+// taps per segment when a FIR is longer than one 16 K-point overlap-save block
+// can hold (> 15361 taps): 8192 minimises the transform work per tap
+// (segments x M / (M - 8192)), one accumulating launch per segment
+constexpr int kFftSegTaps = 8192;
+
 // FFT overlap-save tables of pass p: spectrum of the (gain-scaled) taps in the
 // kernel's digit-reversed order k = k1 + 32 k2 + 1024 k3 -> [k3][k1*32 + k2],
-// pre-divided by M, and the two-level twiddle table.
+// pre-divided by M, and the two-level twiddle table. Taps beyond one block's
+// reach are split into segments, segment j convolving x delayed by j * kFftSegTaps.
 int build_fft(Pass &p) {
     const int M = wpk::FFT_M;
-    const int Tpad = (p.T - 1 + 511) / 512 * 512;
-    if (Tpad >= M - 512) return fail(WP_EUNSUP, "FIR too long for the FFT overlap-save path (taps <= 15361)");
+    int Tpad = (p.T - 1 + 511) / 512 * 512;
+    int segs = 1, seg_taps = p.T;
+    if (Tpad >= M - 512) {
+        seg_taps = kFftSegTaps;
+        segs = (p.T + seg_taps - 1) / seg_taps;
+        Tpad = (seg_taps - 1 + 511) / 512 * 512;
+    }
     double gain = (double)p.pre;
     for (float g : p.post) gain *= (double)g;
-    std::vector<std::complex<double>> h(M, 0.0);
-    for (int i = 0; i < p.T; ++i) h[i] = p.taps[i] * gain / (double)M;
-    host_fft(h);
-    std::vector<float2> Hp(M), tw(256);
-    for (int k3 = 0; k3 < 16; ++k3)
-        for (int k1 = 0; k1 < 32; ++k1)
-            for (int k2 = 0; k2 < 32; ++k2) {
-                const std::complex<double> v = h[k1 + 32 * k2 + 1024 * k3];
-                Hp[k3 * 1024 + k1 * 32 + k2] = make_float2((float)v.real(), (float)v.imag());
-            }
+    std::vector<float2> Hp((size_t)segs * M), tw(256);
+    for (int j = 0; j < segs; ++j) {
+        std::vector<std::complex<double>> h(M, 0.0);
+        for (int i = 0; i < seg_taps && j * seg_taps + i < p.T; ++i)
+            h[i] = p.taps[(size_t)j * seg_taps + i] * gain / (double)M;
+        host_fft(h);
+        for (int k3 = 0; k3 < 16; ++k3)
+            for (int k1 = 0; k1 < 32; ++k1)
+                for (int k2 = 0; k2 < 32; ++k2) {
+                    const std::complex<double> v = h[k1 + 32 * k2 + 1024 * k3];
+                    Hp[(size_t)j * M + k3 * 1024 + k1 * 32 + k2] = make_float2((float)v.real(), (float)v.imag());
+                }
+    }
     for (int i = 0; i < 128; ++i) {
         const double a1 = -2.0 * M_PI * i / M, a2 = -2.0 * M_PI * 128.0 * i / M;
         tw[i] = make_float2((float)std::cos(a1), (float)std::sin(a1));
         tw[128 + i] = make_float2((float)std::cos(a2), (float)std::sin(a2));
     }
-    cudaError_t e = cudaMalloc(&p.d_H, sizeof(float2) * M);
+    cudaError_t e = cudaMalloc(&p.d_H, sizeof(float2) * Hp.size());
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(H)");
-    e = cudaMemcpy(p.d_H, Hp.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(p.d_H, Hp.data(), sizeof(float2) * Hp.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(H)");
     e = cudaMalloc(&p.d_tw, sizeof(float2) * 256);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tw)");
@@ -327,11 +342,12 @@ int build_fft(Pass &p) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tw)");
     p.fft = true;
     p.fft_Tpad = Tpad;
+    p.fft_segs = segs;
     p.Lout = M - Tpad;
     p.grid_cap = wp::sm_count();
     char buf[256];
-    snprintf(buf, sizeof buf, "fft_ols[pre=%g taps=%d post=%zu] M=%d halo=%d block=%d 2 ch/CTA smem=%zu", (double)p.pre, p.T,
-             p.post.size(), M, Tpad, M - Tpad, wp::fft_ols_smem_bytes());
+    snprintf(buf, sizeof buf, "fft_ols[pre=%g taps=%d post=%zu] M=%d halo=%d block=%d 2 ch/CTA smem=%zu segments=%d",
+             (double)p.pre, p.T, p.post.size(), M, Tpad, M - Tpad, wp::fft_ols_smem_bytes(), segs);
     p.desc = buf;
     return WP_OK;
 }
@@ -377,7 +393,11 @@ int finalize_pass(Pass &p) {
         p.tc_nin = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, 2) <= 227 * 1024 ? 2 : 1;
         p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, p.tc_nin) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
     }
-    if (p.S == 0 && p.T > 1 && !(p.fir_flags & WP_FIR_DIRECT) && ((p.fir_flags & WP_FIR_FFT) || !p.fir_tc)) {
+    // FIR-only: FFT overlap-save unless forced direct; a forced-direct FIR beyond the
+    // fused direct kernel's halo (> ~7680 taps) also takes the FFT path
+    const bool direct_fits = (p.T + 7) / 8 * 8 <= wpk::REGION - 9 * wpk::L;
+    if (p.S == 0 && p.T > 1 && (!(p.fir_flags & WP_FIR_DIRECT) || (!p.fir_tc && !direct_fits)) &&
+        ((p.fir_flags & WP_FIR_FFT) || !p.fir_tc)) {
         p.fir_tc = false;
         return build_fft(p);
     }
@@ -735,7 +755,7 @@ int wp_plan_num_passes(const wp_plan *plan) { return plan ? (int)plan->passes.si
 int wp_plan_launches(const wp_plan *plan) {
     if (!plan) return 0;
     int n = 0;
-    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : 1;
+    for (const Pass &p : plan->passes) n += p.kind != Pass::FUSED ? 2 : p.fft ? p.fft_segs : 1;
     return n;
 }
 
@@ -744,7 +764,7 @@ int wp_plan_launches_for(const wp_plan *plan, int64_t channels, int64_t frames) 
     if (!plan) return 0;
     int n = 0;
     for (const Pass &p : plan->passes)
-        n += p.kind != Pass::FUSED ? 2 : 1;
+        n += p.kind != Pass::FUSED ? 2 : p.fft ? p.fft_segs : 1;
     return n;
 }
 
@@ -838,11 +858,16 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.L = p.Lout;
             a.nblk = (N + a.L - 1) / a.L;
             a.total = a.nblk * ((C + 1) / 2);
-            a.H = p.d_H;
             a.tw = p.d_tw;
             const int grid = (int)std::min<long long>(a.total, p.grid_cap);
-            e = wp::launch_fft_ols(a, grid, stream);
-            if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
+            for (int j = 0; j < p.fft_segs; ++j) {
+                // segment j: taps [j K, (j + 1) K) convolve x delayed by j K, added to the first
+                a.H = p.d_H + (size_t)j * wpk::FFT_M;
+                a.delay = (long long)j * kFftSegTaps;
+                a.accumulate = j > 0;
+                e = wp::launch_fft_ols(a, grid, stream);
+                if (e != cudaSuccess) return cuda_fail(e, "fft_ols launch");
+            }
         } else if (p.fir_tc) {
             wpk::FirTcArgs a{};
             a.x = in;

@@ -120,14 +120,14 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         const long long pair = w / a.nblk, blk = w - pair * a.nblk;
         const long long c0 = 2 * pair, c1 = c0 + 1;
         const bool has1 = c1 < a.C;
-        const long long s = blk * a.L - a.Tpad;  // window start sample
+        const long long s = blk * a.L - a.Tpad - a.delay;  // window start sample (delayed input for taps segment > 0)
         const float *x0 = a.x + c0 * a.ldx, *x1 = a.x + (has1 ? c1 : c0) * a.ldx;
         if (t == 0) {
             // warm L2 with the next work item's windows while this block is transformed
             const long long nw = w + gridDim.x;
             if (nw < a.total) {
                 const long long npair = nw / a.nblk, nblk = nw - npair * a.nblk;
-                const long long ns = nblk * a.L - a.Tpad;
+                const long long ns = nblk * a.L - a.Tpad - a.delay;
                 long long lo = ns > 0 ? ns : 0, hi = ns + FM;
                 if (hi > a.N) hi = a.N;
                 lo &= ~3LL;
@@ -209,7 +209,18 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         const long long o0 = blk * a.L - a.Tpad;  // output index of window position 0
         float *q0 = y0 + o0 + t, *q1 = y1 + o0 + t;
         const int j0 = a.Tpad >> 9;  // Tpad is a multiple of 512: n = t + 512 j >= Tpad <=> j >= j0
-        if (o0 + FM <= a.N) {
+        if (a.accumulate) {
+            // taps segment > 0 of a long FIR: add to the previous segments' sum
+            const long long lim = a.N - o0 - t;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j >= j0 && 512LL * j < lim) {
+                    const float2 r = v[brev(j, 5)];
+                    q0[512 * j] += r.x;
+                    if (has1) q1[512 * j] += r.y;
+                }
+            }
+        } else if (o0 + FM <= a.N) {
             // whole block inside the signal: no per-element bound (the common case)
             if (has1) {
 #pragma unroll

@@ -43,6 +43,8 @@ struct FftArgs {
     int Tpad, L;       // halo (multiple of 512, >= taps-1), new outputs per block
     const float2 *H;   // [16][1024] spectrum of the taps, digit-reversed order, x gain / M
     const float2 *tw;  // [256] W_M^n (n < 128), W_M^(128 k) (k < 128)
+    long long delay;   // input delay in samples (taps segment j of a long FIR: j x 8192)
+    int accumulate;    // add to y instead of storing (segments after the first)
 };
 
 }  // namespace wpk

@@ -587,3 +587,38 @@ def test_fuser_passes_and_parity(name):
     for st in bound:
         step = st.apply(step)
     assert np.array_equal(step.samples, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("taps, strategy", [(15361, "auto"), (20001, "auto"), (40961, "fft"), (9001, "direct")])
+def test_long_fir_any_length(taps, strategy):
+    """FIRs longer than one 16 K-point overlap-save block (> 15361 taps) run as
+    accumulating 8192-tap segments (the reference's FFT strategy takes any tap
+    count, engine.py:206-233); a forced-direct FIR past the fused direct kernel's
+    reach also takes the FFT path. Parity vs the direct oracle at the FIR bar."""
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    f = wp.design_fir("lp", taps, 3000, fs=fs)
+    plan = engine.plan_for(wp.Chain([f]).bind(fs).stages, device=0, strategy=strategy)
+    desc = plan.describe()[0]
+    assert desc.startswith("fft_ols"), desc
+    segs = int(desc.split("segments=")[1].split()[0])
+    assert segs == (1 if taps <= 15361 else -(-taps // 8192)), desc
+    rng = np.random.default_rng(taps)
+    w = wp.Wave(rng.standard_normal((3, 50001)), fs)
+    y = wp.apply_fir(f, w, strategy=strategy).samples
+    ref = oracle.fir_direct(f.taps, w.samples)
+    assert oracle.parity_error(y, ref) <= FIR_TOL
+
+
+@pytest.mark.gpu
+def test_iir_then_very_long_fir():
+    """IIR pass followed by a 30000-tap FIR pass (3 accumulating FFT segments)."""
+    fs = 48000
+    stages = [wp.design_butterworth("hp", 2, 50), wp.design_fir("lp", 30001, 5000)]
+    rng = np.random.default_rng(3)
+    w = wp.Wave(rng.standard_normal((2, 60001)), fs)
+    y = wp.pipe(w, wp.Chain(stages)).samples
+    ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
