@@ -298,10 +298,18 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + lay.bars);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 48);
     const uint32_t bar0 = wptc::smem_u32(bars);
+    // per-tile role stamps (tools/trace_lb.py) only in -DLB_TRACE builds: the checks and
+    // stores cost 3 % (cfg3) to 10 % (cfg5) of the pass through the instruction cache
+#ifdef LB_TRACE
 #define LBTR(tile, ev)                                                                \
     do {                                                                              \
         if (a.trace) a.trace[(long long)(tile) * LB_TRACE_EV + (ev)] = ctd::gtimer(); \
     } while (0)
+#else
+#define LBTR(tile, ev) \
+    do {               \
+    } while (0)
+#endif
     // barriers: OP_FULL / OP_EMPTY x 3; E_READY / ACC_EMPTY x 6; C_READY / C_EMPTY x 4;
     // RAW full; L_FULL / L_EMPTY x 4
 #define OPF(s) (bar0 + 8u * (uint32_t)(0 + (s)))

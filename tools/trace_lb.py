@@ -1,4 +1,8 @@
 """Per-tile role timeline of chain_lb (diagnostics): python tools/trace_lb.py [cfg3|cfg5] [seconds]
+Needs a -DLB_TRACE build of the library (the product build compiles the stamps out):
+    python tools/lb_variants.py build traced=-DLB_TRACE
+    WP_LIB=tools/variants/traced/libwpb200.so python tools/trace_lb.py cfg3
+Without one only the untraced time per pass is printed.
 Events (ns, %globaltimer): 0 converter start, 1 operands ready, 2 MMA start, 3 MMAs issued,
 4 look-back start, 5 look-back done, 6 scan done (aggregate published, prefixes in the ring),
 7 epilogue done, 8 scan start (MMAs complete), 9 epilogue has the carry, 10 epilogue has the prefixes,
@@ -45,6 +49,9 @@ plan.execute(x.data_ptr(), y.data_ptr(), C, N, N, N, ws.data_ptr(), nb, st)
 torch.cuda.synchronize()
 _native.set_trace(0, 0)
 t = tr.cpu().numpy().astype(np.float64).reshape(tiles, EV)
+if not (t > 0).any():
+    print("(no stamps: not a -DLB_TRACE build)")
+    sys.exit(0)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan)
 names = ["conv0", "opfull", "mma0", "mma1", "lb0", "lbdone", "scan1", "epi1", "scan0", "carry", "ring", "s_m",
