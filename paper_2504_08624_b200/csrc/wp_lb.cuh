@@ -227,6 +227,26 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// epilogue, last tile of a channel (out of line): staged half rows, stores guarded by the signal end
+static __device__ __noinline__ void store_partial(const unsigned char *stg, float *yr, long long tleft, int vec_y,
+                                                  int wq, int h, int lane) {
+    for (int r = 0; r < 8; ++r) {
+        const int q = lane + 32 * r;
+        const int rr = q >> 3, c4 = q & 7;
+        const float4 v = *reinterpret_cast<const float4 *>(stg + rr * CT_STG_PITCH + 16 * c4);
+        const int oo = 64 * (32 * wq + rr) + 32 * h + 4 * c4;
+        const long long left = tleft - oo;
+        if (vec_y && left >= 4) {
+            __stcs(reinterpret_cast<float4 *>(yr + oo), v);
+        } else {
+            if (left > 0) yr[oo + 0] = v.x;
+            if (left > 1) yr[oo + 1] = v.y;
+            if (left > 2) yr[oo + 2] = v.z;
+            if (left > 3) yr[oo + 3] = v.w;
+        }
+    }
+}
+
 // (a0, a1) += (e0, e1) * s as one packed fp32x2 FMA (FFMA2)
 __device__ __forceinline__ void ffma2(float &a0, float &a1, float e0, float e1, float s) {
     unsigned long long acc = (unsigned long long)__float_as_uint(a0) | ((unsigned long long)__float_as_uint(a1) << 32);
@@ -713,22 +733,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                             __stcs(reinterpret_cast<float4 *>(yr + 64 * (32 * wq + rr) + 32 * h + 4 * c4), v);
                         }
                     } else {
-#pragma unroll 1
-                        for (int r = 0; r < 8; ++r) {
-                            const int q = lane + 32 * r;
-                            const int rr = q >> 3, c4 = q & 7;
-                            const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * CT_STG_PITCH + 16 * c4);
-                            const int oo = 64 * (32 * wq + rr) + 32 * h + 4 * c4;
-                            const long long left = tleft - oo;
-                            if (a.vec_y && left >= 4) {
-                                __stcs(reinterpret_cast<float4 *>(yr + oo), v);
-                            } else {
-                                if (left > 0) yr[oo + 0] = v.x;
-                                if (left > 1) yr[oo + 1] = v.y;
-                                if (left > 2) yr[oo + 2] = v.z;
-                                if (left > 3) yr[oo + 3] = v.w;
-                            }
-                        }
+                        lbd::store_partial(mystg, yr, tleft, a.vec_y, wq, h, lane);
                     }
                     __syncwarp();
                 }
