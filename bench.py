@@ -353,7 +353,9 @@ def main():
             if sampler:
                 sampler.__exit__(None, None, None)
         elapsed_ms = t_start.elapsed_time(t_end)
-        per_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        lt = [a.elapsed_time(b) for a, b in ev]
+        per_launch_ms = statistics.mean(lt)
+        timed.launch_min_median = (min(lt), statistics.median(lt))  # report min and median
         elapsed_ms, per_launch_ms = max_over_ranks([elapsed_ms, per_launch_ms])
         if dist:
             dist.barrier()
@@ -365,6 +367,7 @@ def main():
     y = torch.empty_like(x)
     plan = engine.plan_for(stages, device=local_rank)
     ms_per_step, per_launch_ms, launches, clocks = timed(plan, x, y, C, N, args.steps, args.warmup, clk_gpu=True)
+    launch_min, launch_median = timed.launch_min_median
     units = C * N
     total_units = units * world if args.scaling == "weak" else C_cfg * N
     value = total_units / (ms_per_step / 1e3)
@@ -465,6 +468,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": per_launch_ms,
+                     "launch_ms_min": launch_min, "launch_ms_median": launch_median,
                      "kernel": " + ".join(kernels) + f" ({plan.launches_for(max(C, 1), N)} launch(es) per step)"},
         "e2e": {"value": total_units / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,

@@ -622,3 +622,24 @@ def test_iir_then_very_long_fir():
     y = wp.pipe(w, wp.Chain(stages)).samples
     ref = oracle.pipe(w.samples, wp.Chain(stages).bind(fs).stages)
     assert oracle.parity_error(y, ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+def test_catalog_stages_one_pass():
+    """shelves, peaking EQ, a band-pass and a high-pass windowed-sinc
+    FIR and gains fuse into chain passes and match the oracle."""
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    stages = [wp.design_shelf("lo_shelf", 200, gain_db=4.0), wp.design_peaking(2500, gain_db=-6.0, q=2.0),
+              wp.design_fir("bandpass", 129, (300, 6000)), wp.design_shelf("hi_shelf", 9000, gain_db=-3.0),
+              wp.Gain(0.8), wp.design_fir("highpass", 31, 100)]
+    bound = wp.Chain(stages).bind(fs).stages
+    plan = engine.plan_for(bound, device=0)
+    assert plan.num_passes == 1, plan.describe()
+    assert plan.describe()[0].startswith("chain_lb"), plan.describe()
+    rng = np.random.default_rng(85)
+    w = wp.Wave(rng.standard_normal((4, 90001)), fs)
+    y = wp.pipe(w, wp.Chain(stages)).samples
+    ref = oracle.pipe(w.samples, bound)
+    assert oracle.parity_error(y, ref) <= IIR_TOL
