@@ -314,7 +314,7 @@ int build_fft(Pass &p) {
     }
     double gain = (double)p.pre;
     for (float g : p.post) gain *= (double)g;
-    std::vector<float2> Hp((size_t)segs * M), tw(256);
+    std::vector<float2> Hp((size_t)segs * M), tw(256 + 512 + 2048);
     for (int j = 0; j < segs; ++j) {
         std::vector<std::complex<double>> h(M, 0.0);
         for (int i = 0; i < seg_taps && j * seg_taps + i < p.T; ++i)
@@ -332,13 +332,22 @@ int build_fft(Pass &p) {
         tw[i] = make_float2((float)std::cos(a1), (float)std::sin(a1));
         tw[128 + i] = make_float2((float)std::cos(a2), (float)std::sin(a2));
     }
+    for (int k = 0; k < 32; ++k)  // pass-2 twiddles W_M^(32 bp k), [k][bp]
+        for (int bp = 0; bp < 16; ++bp) {
+            const double an = -2.0 * M_PI * (double)(((long long)32 * bp * k) % M) / M;
+            tw[256 + 16 * k + bp] = make_float2((float)std::cos(an), (float)std::sin(an));
+        }
+    for (int m = 0; m < 2048; ++m) {  // pass-1 anchors W_M^(8 m)
+        const double an = -2.0 * M_PI * 8.0 * m / M;
+        tw[768 + m] = make_float2((float)std::cos(an), (float)std::sin(an));
+    }
     cudaError_t e = cudaMalloc(&p.d_H, sizeof(float2) * Hp.size());
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(H)");
     e = cudaMemcpy(p.d_H, Hp.data(), sizeof(float2) * Hp.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(H)");
-    e = cudaMalloc(&p.d_tw, sizeof(float2) * 256);
+    e = cudaMalloc(&p.d_tw, sizeof(float2) * tw.size());
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tw)");
-    e = cudaMemcpy(p.d_tw, tw.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(p.d_tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tw)");
     p.fft = true;
     p.fft_Tpad = Tpad;

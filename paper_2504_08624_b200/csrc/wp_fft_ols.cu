@@ -33,6 +33,7 @@ namespace {
 constexpr int FM = FFT_M;          // 16384
 constexpr int FT = FFT_THREADS;    // 512
 constexpr int FBUF = 17 * 1024;    // padded complex buffer
+constexpr int FTW = 256 + 512 + 2048;  // twiddles: two-level W_M^n | pass 2 W_M^(32 bp k) [k][bp] | W_M^(8 m)
 
 __constant__ float2 c_w32[16] = {
     {1.000000000e+00f, -0.000000000e+00f}, {9.807852804e-01f, -1.950903220e-01f},
@@ -106,6 +107,37 @@ __device__ __forceinline__ void twiddle32(float2 (&v)[32], const float2 *tw, int
     }
 }
 
+// pass-1 twiddles v[k] *= W_M^(t k): the recurrence w <- w W_M^t, re-anchored every 8
+// powers from the table t8[m] = W_M^(8 m) (t g mod 2048: odd strides, few bank conflicts;
+// the two-level product it replaces read tw[8 g t mod 128] - 16-way conflicts)
+template <bool INV, bool BREV>
+__device__ __forceinline__ void twiddle32_p1(float2 (&v)[32], const float2 *tw, const float2 *t8, int t) {
+    const float2 w1 = twid(tw, t);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        float2 w = g == 0 ? make_float2(1.f, 0.f) : t8[(t * g) & 2047];
+#pragma unroll
+        for (int k = 8 * g; k < 8 * g + 8; ++k) {
+            const int idx = BREV ? brev(k, 5) : k;
+            if (k > 0) v[idx] = INV ? cmulc(v[idx], w) : cmul(v[idx], w);
+            if (k + 1 < 8 * g + 8) w = cmul(w, w1);
+        }
+    }
+}
+
+// pass-2 twiddles v[k] *= W_M^(32 bp k) (INV: conjugate) straight from a table
+// t2[k][bp] (512 entries; bp = thread & 15 varies fastest: conflict-free) - one
+// complex multiply per point instead of the recurrence's two
+template <bool INV, bool BREV>
+__device__ __forceinline__ void twiddle32_tab(float2 (&v)[32], const float2 *t2, int bp) {
+#pragma unroll
+    for (int k = 1; k < 32; ++k) {
+        const int idx = BREV ? brev(k, 5) : k;
+        const float2 w = t2[16 * k + bp];
+        v[idx] = INV ? cmulc(v[idx], w) : cmul(v[idx], w);
+    }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
@@ -113,7 +145,9 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
     float2 *buf = fsm;
     float2 *tws = fsm + FBUF;
     const int t = threadIdx.x;
-    for (int i = t; i < 256; i += FT) tws[i] = a.tw[i];
+    for (int i = t; i < FTW; i += FT) tws[i] = a.tw[i];
+    const float2 *tw2 = tws + 256;
+    const float2 *tw8 = tws + 768;
     __syncthreads();
     const int k1p = t >> 4, bp = t & 15;  // pass-2 coordinates of this thread
     for (long long w = blockIdx.x; w < a.total; w += gridDim.x) {
@@ -160,7 +194,7 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         }
         // ---- forward pass 1: DFT32 over j, twiddle W_M^(t k1) -> buf[k1*512 + t] ----
         fft_reg<32, false>(v);
-        twiddle32<false, true>(v, tws, t);
+        twiddle32_p1<false, true>(v, tws, tw8, t);
         __syncthreads();  // previous block's last reads of buf are done
 #pragma unroll
         for (int k1 = 0; k1 < 32; ++k1) buf[k1 * 512 + t] = v[brev(k1, 5)];
@@ -169,7 +203,7 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = buf[k1p * 512 + bp + 16 * c];
         fft_reg<32, false>(v);
-        twiddle32<false, true>(v, tws, 32 * bp);
+        twiddle32_tab<false, true>(v, tw2, bp);
         __syncthreads();
 #pragma unroll
         for (int k2 = 0; k2 < 32; ++k2) buf[17 * (k1p * 32 + k2) + bp] = v[brev(k2, 5)];
@@ -193,7 +227,7 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         // ---- inverse pass 2: conj twiddle, IDFT32 over k2 -> c ----
 #pragma unroll
         for (int k2 = 0; k2 < 32; ++k2) v[k2] = buf[17 * (k1p * 32 + k2) + bp];
-        twiddle32<true, false>(v, tws, 32 * bp);
+        twiddle32_tab<true, false>(v, tw2, bp);
         fft_reg<32, true>(v);
         __syncthreads();
 #pragma unroll
@@ -202,7 +236,7 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
         // ---- inverse pass 1: conj twiddle W_M^(t k1), IDFT32 over k1 -> j ----
 #pragma unroll
         for (int k1 = 0; k1 < 32; ++k1) v[k1] = buf[k1 * 512 + t];
-        twiddle32<true, false>(v, tws, t);
+        twiddle32_p1<true, false>(v, tws, tw8, t);
         fft_reg<32, true>(v);
         // outputs n = t + 512 j >= Tpad of this block (1/M folded into H)
         float *y0 = a.y + c0 * a.ldy, *y1 = a.y + (has1 ? c1 : c0) * a.ldy;
@@ -253,7 +287,7 @@ __global__ void __launch_bounds__(FT, 1) fft_ols_kernel(const FftArgs a) {
 
 namespace wp {
 
-size_t fft_ols_smem_bytes() { return sizeof(float2) * (size_t)(wpk::FBUF + 256); }
+size_t fft_ols_smem_bytes() { return sizeof(float2) * (size_t)(wpk::FBUF + wpk::FTW); }
 
 cudaError_t launch_fft_ols(const wpk::FftArgs &a, int grid, cudaStream_t st) {
     const size_t smem = fft_ols_smem_bytes();
