@@ -383,7 +383,10 @@ int finalize_pass(Pass &p) {
         // IIR-only: small calls keep the fused chunked scan (one launch, exact
         // per-chunk recurrence for the known-answer cases)
         p.lb_large = true;
-        p.lb_min_tiles = lb_forced() ? 0 : 2LL * wp::sm_count();
+        // measured crossover (tools/iir_small_probe.py): chain_lb is faster from ~16 tiles
+        // for >= 3 sections and from ~64 tiles for 1-2 sections; below that the single
+        // fused launch wins and keeps its exact per-chunk recurrence for the KAT cases
+        p.lb_min_tiles = lb_forced() ? 0 : (p.S >= 3 ? 16 : 64);
         if (p.T == 1) {
             // a 1-tap FIR is a gain: the fused kernel takes it as a post gain
             p.post.push_back((float)p.taps[0]);

@@ -327,8 +327,10 @@ def test_fir_tensor_core_zeros_and_tail():
                   wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, (32, 5760000), "chain_lb"),  # cfg3
         (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1024, 14400000), "chain_lb"),      # cfg5
         (lambda: _bench_chain(), 44100, (2, 88200), "chain_lb"),                                    # 8 SOS: one pass
-        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (4, 48000), "fused"),                 # small IIR
-        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, (2, 441000), "fused"),                # cfg1
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1, 16384), "fused"),                 # tiny IIR
+        (lambda: [wp.design_butterworth("lp", 4, 1000)], 48000, (2, 96000), "fused"),                 # small, 2 SOS
+        (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (4, 48000), "chain_lb"),              # small, 4 SOS
+        (lambda: [wp.design_butterworth("lp", 4, 1000)], 44100, (2, 441000), "chain_lb"),             # cfg1
         (lambda: [wp.design_fir("lp", 101, 1000, "hamming")], 48000, (8, 2880000), "fir_tc"),          # cfg2
         (lambda: [wp.design_fir("lp", 4096, 2000, "hamming")], 48000, (128, 28800000), "fft_ols"),     # cfg4
     ],
