@@ -73,13 +73,19 @@ def _chain(stages):
     return Chain([stages])
 
 
-def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: str = "host"):
+_PIN_MAX_BYTES = 4 << 30  # a gathered output larger than this is not page-locked
+
+
+def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: str = "host", out=None):
     """Filter ``wave`` through ``stages`` with its channels split across
     ``devices`` (default: every visible CUDA device).
 
-    gather="host": returns one host-resident Wave (pinned float32), the blocks
-    copied back asynchronously from each device. gather=None: returns the
-    list of device-resident per-block Waves (no copies at all)."""
+    gather="host": returns one host-resident Wave, each device's block copied
+    back as soon as it is done. ``out`` (optional): a CPU float32 tensor
+    ``[C, N]`` to gather into (pinned: asynchronous copies); without it the
+    gather buffer is pinned only up to 4 GiB (cfg5's 59 GB output would
+    otherwise page-lock all of it). gather=None: returns the list of
+    device-resident per-block Waves (no copies at all)."""
     torch = _torch()
     from ._native import _require_cuda
 
@@ -111,10 +117,15 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
     shards = _run_segments(shards, chain, lambda peaks: max(peaks))
     if gather is None:
         return [w for _, _, w in shards]
-    out = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
+    if out is None:
+        out = torch.empty((C, N), dtype=torch.float32, pin_memory=C * N * 4 <= _PIN_MAX_BYTES)
+    elif (not isinstance(out, torch.Tensor) or out.device.type != "cpu" or out.dtype != torch.float32
+          or tuple(out.shape) != (C, N)):
+        raise InvalidArgument(f"out must be a CPU float32 tensor of shape {(C, N)}")
+    pinned = out.is_pinned()
     for (c0, c1), dev, w in shards:
         with torch.cuda.device(dev):
-            out[c0:c1].copy_(w.tensor(), non_blocking=True)
+            out[c0:c1].copy_(w.tensor(), non_blocking=pinned)
     for _, dev, _ in shards:
         torch.cuda.synchronize(dev)
     return Wave.from_tensor(out, wave.fs)

@@ -147,3 +147,39 @@ def test_pinned_source_chain_with_normalize_is_not_streamed_per_block():
     got = lazy.numpy32().astype(np.float64)
     assert np.array_equal(got, ref)
     assert np.max(np.abs(got)) == pytest.approx(1.0, rel=1e-6)
+
+
+@pytest.mark.gpu
+def test_shard_pipe_into_caller_buffer():
+    """gather into a caller-provided host tensor (pinned or pageable), as a
+    59 GB cfg5 output should be, instead of a fresh page-locked buffer."""
+    import torch
+
+    fs = 48000
+    w = wp.white_noise(0.5, 5, fs, seed=11)
+    chain = wp.Chain([wp.design_butterworth("lp", 8, 2000)])
+    ref = (w | chain).samples
+    for pin in (True, False):
+        out = torch.empty((5, w.frames), dtype=torch.float32, pin_memory=pin)
+        got = wp.shard_pipe(w, chain, devices=[0, 0], out=out)
+        assert np.array_equal(got.samples, ref)
+        assert np.array_equal(out.numpy().astype(np.float64), ref)
+    with pytest.raises(wp.InvalidArgument):
+        wp.shard_pipe(w, chain, devices=[0], out=torch.empty((4, w.frames)))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not __import__("torch").cuda.is_available() or __import__("torch").cuda.device_count() < 2,
+                    reason="needs >= 2 visible GPUs")
+def test_shard_pipe_real_devices():
+    """Channels split over every visible GPU (one stream each), bit-identical to one GPU."""
+    import torch
+
+    fs = 48000
+    n = torch.cuda.device_count()
+    w = wp.white_noise(1.0, 4 * n + 1, fs, seed=12)
+    chain = wp.Chain([wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
+                      wp.design_fir("lp", 101, 15000), wp.Gain(0.5)])
+    ref = (w | chain).samples
+    got = wp.shard_pipe(w, chain, devices=list(range(n))).samples
+    assert np.array_equal(got, ref)
