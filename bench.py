@@ -52,6 +52,11 @@ CONFIGS = {
                  workload="32-channel 48 kHz 120 s chain: high-pass Butterworth | low-pass Chebyshev-I | FIR | gain via the pipe operator (fused)"),
     "cfg4": dict(C=128, fs=48000, dur=600.0, workload="128-channel 48 kHz 10 min through a 4096-tap FIR"),
     "cfg5": dict(C=1024, fs=48000, dur=300.0, workload="1024-channel 48 kHz 5 min 8th-order SOS IIR cascade"),
+    # not a BASELINE config: the reference's own pinned interface-comparison chain
+    # (pkg/src/wavepipe/bench.py:93-100, 2 Butterworth-4 + 2 Chebyshev-4 = 8 SOS) at
+    # cfg3's size, fused into ONE pass
+    "bench_chain": dict(C=32, fs=44100, dur=120.0,
+                        workload="32-channel 44.1 kHz 120 s: the reference's pinned 8-SOS bench chain (one pass)"),
 }
 
 
@@ -67,6 +72,9 @@ def stages_for(name, wp):
         return [wp.design_fir("lp", 4096, 2000, "hamming")]
     if name == "cfg5":
         return [wp.design_butterworth("lp", 8, 2000)]
+    if name == "bench_chain":
+        return [wp.design_butterworth("lowpass", 4, 1000.0), wp.design_butterworth("lowpass", 4, 1200.0),
+                wp.design_chebyshev1("lowpass", 4, 1.0, 2000.0), wp.design_chebyshev1("lowpass", 4, 1.0, 2400.0)]
     raise SystemExit(f"unknown config {name}")
 
 

@@ -269,6 +269,23 @@ bool lb_enabled() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
     return !(v && std::string(v) == "cuda");
 }
+// sections per chain_lb pass for a run of `total` IIR sections. One pass costs
+// more than linearly in the state size past 4 sections (D = 16: the D^2 scan and
+// look-back work and 2 x the E s FMAs), so measured on the reference's 8-SOS
+// bench chain (32 x 5.29 M): one 8-section pass 1.71 ms, 4 + 4 0.92 ms, 5 + 3
+// 1.05, 6 + 2 1.25, 3 + 3 + 2 1.18; five sections: one pass 0.65 vs 3 + 2 0.76.
+// Hence: up to 5 sections in one pass, more split into balanced passes of <= 4.
+// WP_LB_MAXS=n forces at most n per pass (A/B).
+int lb_max_sections(int total) {
+    const char *v = std::getenv("WP_LB_MAXS");
+    if (v) {
+        const int n = std::atoi(v);
+        if (n >= 1 && n <= 8) return n;
+    }
+    if (total <= 5) return 8;
+    const int passes = (total + 3) / 4;
+    return (total + passes - 1) / passes;
+}
 bool lb_forced() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
     return v && std::string(v) == "lb";
@@ -597,6 +614,21 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
         cur = Pass();
     };
     const bool lti = lb_enabled();
+    // IIR sections (non-identity) in the LTI run (stages up to the next Normalize) of each stage
+    std::vector<int> run_sections(n_stages > 0 ? n_stages : 1, 0);
+    for (int a = 0; a < n_stages;) {
+        int b = a, tot = 0;
+        while (b < n_stages && stages[b].kind != WP_STAGE_NORMALIZE) {
+            if (stages[b].kind == WP_STAGE_IIR && stages[b].coef)
+                for (int k = 0; k < stages[b].n; ++k) {
+                    const double *r = stages[b].coef + 5 * k;
+                    if (!(r[0] == 1.0 && r[1] == 0.0 && r[2] == 0.0 && r[3] == 0.0 && r[4] == 0.0)) ++tot;
+                }
+            ++b;
+        }
+        for (int q = a; q < b; ++q) run_sections[q] = tot;
+        a = b + 1;
+    }
     for (int si = 0; si < n_stages; ++si) {
         const wp_stage &st = stages[si];
         if (lti) {
@@ -627,7 +659,7 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                 }
                 if (keep.empty()) continue;
                 for (size_t idx = 0; idx < keep.size(); ++idx) {
-                    if (cur.S == 8 || (cur.T > 0 && cur.T - 1 > lbh)) close();
+                    if (cur.S == lb_max_sections(run_sections[si]) || (cur.T > 0 && cur.T - 1 > lbh)) close();
                     for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * keep[idx] + j]);
                     cur.S += 1;
                     cur.prec_flag |= st.flags & (WP_IIR_PREC_F32 | WP_IIR_PREC_F64);

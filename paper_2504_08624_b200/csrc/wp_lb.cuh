@@ -65,6 +65,9 @@
 
 namespace wpk {
 
+#ifndef LB_GL_MAXD
+#define LB_GL_MAXD 16  // lane-minor M^l table for every state size (8: only up to 4 sections)
+#endif
 constexpr int LB_THREADS = 512;
 constexpr int LB_CONV = 160;   // converter threads (warps 2..6)
 constexpr int LB_QMAX = 14;    // float4 of the window per converter thread (W <= 8960)
@@ -102,7 +105,7 @@ struct LbArgs {
 // Ep[32][D][2] (E[2q][d], E[2q+1][d] pairs) | Mp[7][D][DP] (M^(2^b)) | Wt[4][D][DP] (M^(32 w)) | Gl[LT][32] (M^l, lane-minor; D <= 8 only)
 __host__ __device__ constexpr int lb_de(int D) { return D <= 8 ? 8 : 16; }
 __host__ __device__ constexpr int lb_dp(int D) { return (D + 3) & ~3; }
-__host__ __device__ constexpr int lb_has_gl(int D) { return D <= 8; }
+__host__ __device__ constexpr int lb_has_gl(int D) { return D <= LB_GL_MAXD; }
 __host__ __device__ constexpr int lb_tab_floats(int D) {
     return 64 * D + 11 * D * lb_dp(D) + (lb_has_gl(D) ? 32 * lt_size(D) : 0);
 }

@@ -326,7 +326,8 @@ def test_fir_tensor_core_zeros_and_tail():
         (lambda: [wp.design_butterworth("hp", 4, 100), wp.design_chebyshev1("lp", 4, 1.0, 8000),
                   wp.design_fir("lp", 101, 15000), wp.Gain(0.5)], 48000, (32, 5760000), "chain_lb"),  # cfg3
         (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1024, 14400000), "chain_lb"),      # cfg5
-        (lambda: _bench_chain(), 44100, (2, 88200), "chain_lb"),                                    # 8 SOS: one pass
+        (lambda: _bench_chain()[:2] + [wp.design_peaking(1000, gain_db=2.0)], 44100, (2, 88200),
+         "chain_lb"),                                                                                # 5 SOS: one pass
         (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (1, 16384), "fused"),                 # tiny IIR
         (lambda: [wp.design_butterworth("lp", 4, 1000)], 48000, (2, 96000), "fused"),                 # small, 2 SOS
         (lambda: [wp.design_butterworth("lp", 8, 2000)], 48000, (4, 48000), "chain_lb"),              # small, 4 SOS
@@ -561,12 +562,14 @@ def test_plan_execute_in_cuda_graph():
 @pytest.mark.parametrize("name", ["bench_chain_8sos", "fir_then_iir", "iir_fir241_gain", "two_firs_iir",
                                   "iir_long_fir_split"])
 def test_fuser_passes_and_parity(name):
-    """The reference's pinned 8-SOS chain (bench.py:93-100) and its mixed FIR ->
-    IIR chain (test_chain.py:167-173) run as ONE pass; a FIR too long for the
-    single-pass kernel gets its own FIR-only pass after the IIR pass."""
+    """The reference's mixed FIR -> IIR chain (test_chain.py:167-173) runs as ONE
+    pass, its pinned 8-SOS chain (bench.py:93-100) as two balanced 4-section
+    passes (measured faster than one 8-section pass; test_eight_sections_one_pass
+    covers the single-pass form); a FIR too long for the single-pass kernel gets
+    its own FIR-only pass after the IIR pass."""
     fs = 44100 if name in ("bench_chain_8sos", "fir_then_iir") else 48000
     chains = {
-        "bench_chain_8sos": (_bench_chain(), 1),
+        "bench_chain_8sos": (_bench_chain(), 2),  # 4 + 4 sections: 1.86x faster than one 8-section pass
         "fir_then_iir": ([wp.design_fir("lowpass", 33, 4000), wp.design_peaking(1000, gain_db=2.0)], 1),
         "iir_fir241_gain": ([wp.design_chebyshev1("lp", 4, 1.0, 5000), wp.design_fir("lp", 241, 9000), wp.Gain(0.7)], 1),
         "two_firs_iir": ([wp.design_fir("lp", 61, 9000), wp.design_butterworth("hp", 2, 80),
@@ -645,3 +648,32 @@ def test_catalog_stages_one_pass():
     y = wp.pipe(w, wp.Chain(stages)).samples
     ref = oracle.pipe(w.samples, bound)
     assert oracle.parity_error(y, ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maxs, passes", [(8, 1), (5, 2), (3, 3)])
+def test_eight_sections_one_pass(maxs, passes, monkeypatch):
+    """WP_LB_MAXS caps the sections per chain_lb pass: the reference's 8-SOS bench
+    chain as ONE 16-state pass (D = 16 kernel), as 5 + 3 and as 3 + 3 + 2, all
+    within the IIR bar of the oracle."""
+    from paper_2504_08624_b200 import engine
+
+    monkeypatch.setenv("WP_LB_MAXS", str(maxs))
+    monkeypatch.setenv("WP_CHAIN_IMPL", "lb")  # chain_lb even for the small 2-section remainder
+    fs = 44100
+    bound = wp.Chain(_bench_chain()).bind(fs).stages
+    plan = _native.Plan(tuple(engine._entry(s) for s in bound))  # uncached: the env var applies
+    assert plan.num_passes == passes, plan.describe()
+    assert all(d.startswith("chain_lb") for d in plan.describe_for(3, 90001)), plan.describe()
+    rng = np.random.default_rng(maxs)
+    x = rng.standard_normal((3, 90001)).astype(np.float32)
+    import torch
+
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    nb = plan.workspace_bytes(3, 90001)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    plan.execute(xd.data_ptr(), yd.data_ptr(), 3, 90001, 90001, 90001, ws.data_ptr(), nb,
+                 torch.cuda.current_stream().cuda_stream)
+    ref = oracle.pipe(x.astype(np.float64), bound)
+    assert oracle.parity_error(yd.cpu().numpy().astype(np.float64), ref) <= IIR_TOL
