@@ -1,9 +1,11 @@
 // C ABI of libwpb200.so (declarations in include/wavepipe_b200.h).
 //
 // A plan turns the reference's stage list (Chain.stages, chain.py:27-41) into
-// fused passes and precomputes, in float64 on the host, every transfer matrix
-// the chunked IIR scan needs. Executing a plan issues one kernel per pass
-// (plus a 4-byte counter memset), never allocates and never synchronizes.
+// fused passes (each run of IIR / FIR / gain stages is one LTI pass while it
+// fits chain_lb) and precomputes, in long double on the host, every table the
+// kernels need. Executing a plan issues one kernel per pass (plus a small
+// stream-ordered memset of the look-back records / tile counter), never
+// allocates and never synchronizes.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-#include "../paper_2504_08624_b200/csrc/wp_chain_tc.cuh"
+#include "../paper_2504_08624_b200/csrc/wp_common.cuh"  // (round-1 probe: built against wp_chain_tc.cuh, since removed)
 
 using namespace wpk;
 constexpr int D = 8;
