@@ -3,6 +3,7 @@
 
     python tools/lb_variants.py build NAME=-DLB_EG=2,-DLB_FFMA2=0 ...
     python tools/lb_variants.py build NAME@REV=...    # wp_lb.cu/.cuh (and wp_internal.h) as of git REV
+    python tools/lb_variants.py build NAME%wp_fir_tc.cu=-DX   # a variant of another translation unit
     python tools/lb_variants.py run cfg3          # on the GPU: every built variant, tools/trace_lb.py timing
 
 Variants land in tools/variants/<NAME>/libwpb200.so (git-ignored, travels with gpurun)."""
@@ -23,12 +24,14 @@ def build(specs):
     objs = sorted(glob.glob(os.path.join(b.OBJ_DIR, "*.o")))
     for spec in specs:
         name, _, flags = spec.partition("=")
+        name, _, srcfile = name.partition("%")  # NAME%wp_fir_tc.cu=...: a variant of another source file
+        srcfile = srcfile or "wp_lb.cu"
         name, _, rev = name.partition("@")
         flags = [f for f in flags.split(",") if f]
         out = os.path.join(VDIR, name)
         os.makedirs(out, exist_ok=True)
-        obj = os.path.join(out, "wp_lb.o")
-        src = os.path.join(b.CSRC, "wp_lb.cu")
+        obj = os.path.join(out, srcfile[:-3] + ".o")
+        src = os.path.join(b.CSRC, srcfile)
         if rev:
             # the chain kernel sources of an older revision, next to the current other headers
             sdir = os.path.join(out, "csrc")
@@ -44,8 +47,7 @@ def build(specs):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise SystemExit(r.stderr)
-        spills = [l for l in r.stderr.splitlines() if "chain_lb_kernelILi8ELi2" in l]
-        link = [o for o in objs if not o.endswith("wp_lb.o")] + [obj]
+        link = [o for o in objs if not o.endswith(os.path.basename(obj))] + [obj]
         r = subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", os.path.join(out, "libwpb200.so"), *link, "-lpthread"],
                            capture_output=True, text=True)
         if r.returncode:
