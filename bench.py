@@ -351,12 +351,19 @@ def main():
             launches0 = _native.launch_count()
             t_start.record(stream)
             for i in range(steps):
-                ev[i][0].record(stream)
                 step()
-                ev[i][1].record(stream)
             t_end.record(stream)
             torch.cuda.synchronize()
             launches = _native.launch_count() - launches0
+            # per-step events in a second, separate run (SURVEY §8(d) min / median): an
+            # event between two passes stops the next kernel's prologue from overlapping
+            # the previous one's tail (programmatic dependent launch), so the headline
+            # above times the K passes back to back
+            for i in range(steps):
+                ev[i][0].record(stream)
+                step()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
         finally:
             if sampler:
                 sampler.__exit__(None, None, None)

@@ -288,6 +288,10 @@ int lb_max_sections(int total) {
     const int passes = (total + 3) / 4;
     return (total + passes - 1) / passes;
 }
+int env_int(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
 bool lb_forced() {
     const char *v = std::getenv("WP_CHAIN_IMPL");
     return v && std::string(v) == "lb";
@@ -368,6 +372,8 @@ int build_fft(Pass &p) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tw)");
     e = cudaMemcpy(p.d_tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tw)");
+    e = wp::fft_ols_prepare();  // kernel attribute, once per plan (not per execute)
+    if (e != cudaSuccess) return cuda_fail(e, "fft_ols attribute");
     p.fft = true;
     p.fft_Tpad = Tpad;
     p.fft_segs = segs;
@@ -421,7 +427,14 @@ int finalize_pass(Pass &p) {
         // double-buffered fp32 windows up to 129 taps, one window buffer up to 257 taps (the
         // B image grows with the taps); beyond that FFT overlap-save is the faster path anyway
         // (profiles/r2_fir_crossover.md: fir_tc 0.19-0.21 ms vs fft_ols 0.31 ms per pass)
-        p.tc_nin = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, 2) <= 227 * 1024 ? 2 : 1;
+        // window/operand slots in the ring: as many as shared memory holds (<= 4); WP_FIR_NIN caps it (A/B)
+        const int nin_cap = env_int("WP_FIR_NIN", 4);
+        p.tc_nin = 1;
+        for (int n = std::min(4, std::max(1, nin_cap)); n > 1; --n)
+            if (wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, n) <= 227 * 1024) {
+                p.tc_nin = n;
+                break;
+            }
         p.fir_tc = wp::fir_tc_smem_bytes(p.tc_W, p.tc_K, p.tc_nin) <= 227 * 1024 && p.tc_W <= 10 * 4 * 256;
     }
     // FIR-only: FFT overlap-save unless forced direct; a forced-direct FIR beyond the
@@ -467,7 +480,7 @@ int finalize_pass(Pass &p) {
         p.Lout = wpk::TC_TOUT;
         char buf[256];
         snprintf(buf, sizeof buf,
-                 "fir_tc[pre=%g taps=%d K=%d post=%zu] tcgen05 f16x3 M128xN64 SW128 tile=%d smem=%zu occ=%d windows=%d",
+                 "fir_tc[pre=%g taps=%d K=%d post=%zu] tcgen05 f16x3 M128xN64 SW128 tile=%d smem=%zu occ=%d slots=%d",
                  (double)p.pre, p.T, p.tc_K, p.post.size(), wpk::TC_TOUT, p.smem, occ, p.tc_nin);
         p.desc = buf;
         return WP_OK;
@@ -932,12 +945,11 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.pre_gain = p.pre;
             a.n_post = (int)p.post.size();
             for (int j = 0; j < a.n_post; ++j) a.post[j] = p.post[j];
-            a.counter = counter;
             a.vec_x = (ld_in % 4 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
             a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+            a.trace = (g_trace && g_trace_entries >= (size_t)a.total_tiles * wpk::FT_TRACE_EV) ? g_trace : nullptr;
+            if (a.total_tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
             const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
-            e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
-            if (e != cudaSuccess) return cuda_fail(e, "memset(counter)");
             e = wp::launch_fir_tc(a, grid, p.smem, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fir_tc launch");
         } else {

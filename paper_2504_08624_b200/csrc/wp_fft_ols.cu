@@ -289,10 +289,13 @@ namespace wp {
 
 size_t fft_ols_smem_bytes() { return sizeof(float2) * (size_t)(wpk::FBUF + wpk::FTW); }
 
+cudaError_t fft_ols_prepare() {
+    return cudaFuncSetAttribute(wpk::fft_ols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fft_ols_smem_bytes());
+}
+
 cudaError_t launch_fft_ols(const wpk::FftArgs &a, int grid, cudaStream_t st) {
-    const size_t smem = fft_ols_smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(wpk::fft_ols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    const size_t smem = fft_ols_smem_bytes();  // attribute set at plan build (fft_ols_prepare)
     wpk::fft_ols_kernel<<<grid, wpk::FFT_THREADS, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();

@@ -25,8 +25,9 @@
 //   warps 2-9 convert window -> swizzled fp16 hi/lo operands
 //   warps 10-13 epilogue: TMEM -> registers -> padded smem staging ->
 //            coalesced stores (runs concurrently with the next conversion)
-//   double buffers: fp32 window, fp16 operands, TMEM accumulators
-//   (2 x 128 columns); one padded output staging tile.
+//   a ring of 2-4 slots (each: the fp32 window, then in place its fp16 hi | lo
+//   operands until the MMAs have read them), TMEM accumulators (2 x 128
+//   columns), one padded output staging tile.
 #include <cuda_fp16.h>
 
 #include "wp_internal.h"
@@ -41,6 +42,51 @@ constexpr int kConv = 256;        // converter threads (warps 2..9)
 constexpr int kEpi = 128;         // epilogue threads (warps 10..13, one per TMEM lane quarter)
 constexpr int kMaxQ = 10;         // float4 of the window per converter thread (W <= 10240)
 constexpr int kStagePitch = 272;  // bytes per staged output row (256 + 16 pad)
+
+// Upper-bound diagnostics (tools/lb_variants.py, never in the product build): FT_UB_NOLOAD
+// skips the window copies, FT_UB_NOCONV the operand conversion, FT_UB_NOMMA the MMAs,
+// FT_UB_NOSTORE the output stores. Each leaves the pipeline's synchronisation intact.
+#ifndef FT_NA
+#define FT_NA 2  // TMEM accumulator stages (128 columns each)
+#endif
+// FT_TRACE: per-tile stage stamps (%globaltimer) into a.trace (tools/trace_fir.py)
+#ifdef FT_TRACE
+#define FTTR(i, ev)                                                                                       \
+    do {                                                                                                  \
+        if (a.trace) a.trace[(first + (long long)(i) * stride) * FT_TRACE_EV + (ev)] = ctd_gtimer();     \
+    } while (0)
+#else
+#define FTTR(i, ev) \
+    do {            \
+    } while (0)
+#endif
+#ifndef FT_MMA_ORDER
+#define FT_MMA_ORDER 0  // 1: all hi MMAs, then all lo MMAs (A/B)
+#endif
+#ifndef FT_UB_MMA
+#define FT_UB_MMA 0  // upper bound: 1 issues only the N=128 hi MMAs, 2 only the N=64 lo MMAs
+#endif
+#ifndef FT_UB_ALIGN
+#define FT_UB_ALIGN 0  // upper bound: 1 keeps every A start in the first swizzle row, 2 also B
+#endif
+#ifndef FT_BOFF
+#define FT_BOFF 0  // descriptor matrix base offset = start row within the swizzle atom (A/B)
+#endif
+#ifndef FT_PDL
+#define FT_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail)
+#endif
+#ifndef FT_UB_NOLOAD
+#define FT_UB_NOLOAD 0
+#endif
+#ifndef FT_UB_NOCONV
+#define FT_UB_NOCONV 0
+#endif
+#ifndef FT_UB_NOMMA
+#define FT_UB_NOMMA 0
+#endif
+#ifndef FT_UB_NOSTORE
+#define FT_UB_NOSTORE 0
+#endif
 
 __device__ __forceinline__ uint32_t swz128(uint32_t byte) { return byte ^ (((byte >> 7) & 7u) << 4); }
 
@@ -70,15 +116,23 @@ __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ctd_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct Geo {
     long long c, n0, start;  // channel, first output, window start sample
     long long lo, hi;        // bulk-copied sample range [lo, hi)
 };
 
+// tile < 2^31 (checked on the host): 32-bit division keeps the three inlined copies small
 __device__ __forceinline__ Geo geo(const FirTcArgs &a, long long tile) {
     Geo g;
-    g.c = tile % a.C;
-    g.n0 = (tile / a.C) * (long long)TC_TOUT;
+    const uint32_t t = (uint32_t)tile, C = (uint32_t)a.C;
+    g.c = t % C;
+    g.n0 = (long long)(t / C) * (long long)TC_TOUT;
     g.start = g.n0 - a.Tp;
     g.lo = g.start > 0 ? g.start : 0;
     const long long nv = a.vec_x ? (a.N & ~3LL) : 0;  // vector-copyable prefix
@@ -86,6 +140,32 @@ __device__ __forceinline__ Geo geo(const FirTcArgs &a, long long tile) {
     if (hi > nv) hi = nv;
     g.hi = hi > g.lo ? hi : g.lo;
     return g;
+}
+
+// Edge tile (signal start/end, or an unaligned channel): complete the fp32 window in
+// place - zeros outside [0, N), samples the bulk copy did not cover read from global -
+// so the converters' hot loop has no per-element bounds (out of line: rare, and kept
+// out of the instruction cache's way).
+__device__ __noinline__ void fill_window(float *win, const float *xr, long long start, long long lo, long long hi,
+                                         long long N, int W, int ct) {
+    for (int k = ct; k < W; k += kConv) {
+        const long long p = start + k;
+        if (p >= lo && p < hi) continue;  // bulk-copied
+        win[k] = (p >= 0 && p < N) ? __ldg(xr + p) : 0.f;
+    }
+}
+
+// Last tile of a channel, or an unaligned output: guarded scalar copy-out of the staging tile.
+__device__ __noinline__ void store_partial(const unsigned char *stg, float *yr, long long left, int et) {
+    for (int q = et; q < TC_TOUT / 4; q += kEpi) {
+        const int r = q >> 4, c4 = q & 15;
+        const float4 v = *reinterpret_cast<const float4 *>(stg + r * kStagePitch + 16 * c4);
+        const long long p0 = 4LL * q;
+        if (p0 + 0 < left) yr[p0 + 0] = v.x;
+        if (p0 + 1 < left) yr[p0 + 1] = v.y;
+        if (p0 + 2 < left) yr[p0 + 2] = v.z;
+        if (p0 + 3 < left) yr[p0 + 3] = v.w;
+    }
 }
 
 }  // namespace
@@ -100,34 +180,40 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
     const int nk = a.K / 16;
     // ---- shared memory carve-up ----
     const uint32_t opBytes = ((uint32_t)a.W * 2u + 1023u) & ~1023u;  // one fp16 window
-    const uint32_t inBytes = ((uint32_t)a.W * 4u + 1023u) & ~1023u;
+    // a slot holds a tile's fp32 window, then - converted in place - its fp16 hi | lo
+    // operands until the MMAs have read them; a.nin (<= 4) slots form the ring
+    const uint32_t slotBytes = 2u * opBytes;
     const uint32_t stgBytes = (128u * kStagePitch + 1023u) & ~1023u;
     const uint32_t bBytes = (uint32_t)((a.K + 63) / 64) * 8192u;  // one split of B
-    // fp32 windows: double-buffered, or one buffer (a.nin == 1) when the taps' B image
-    // needs the room (T > 129): the converters free it as soon as it is in registers
-    unsigned char *inbuf0 = smem, *inbuf1 = smem + (a.nin > 1 ? inBytes : 0u);
-    unsigned char *stg = smem + (uint32_t)a.nin * inBytes;  // output staging (padded rows)
-    unsigned char *op = stg + stgBytes;       // [stage][hi, lo]
-    unsigned char *bimg = op + 4 * opBytes;  // [hi, lo]
+    unsigned char *stg = smem + (uint32_t)a.nin * slotBytes;  // output staging (padded rows)
+    unsigned char *bimg = stg + stgBytes;                     // [hi, lo]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(bimg + 2 * bBytes);
-    // bars: in_full[2], in_empty[2], op_full[2], op_empty[2], acc_full[2], acc_empty[2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 12);
+    // bars: full[4], free[4], op_full[4], acc_full[4], acc_empty[4]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 20);
     float *red = reinterpret_cast<float *>(tmem_slot + 1);  // [8]
-    float *scl = red + 8;                                    // per-stage scale [2]
+    // per-tile window scale, a ring of nin + FT_NA entries: the converter of tile t
+    // may run nin tiles ahead of the MMA of tile t - nin, which waited for the
+    // epilogue of tile t - nin - FT_NA, the previous reader of entry t % (nin + FT_NA)
+    float *scl = red + 8;  // [8]
+    const int nscl = a.nin + FT_NA;
     const uint32_t bar0 = wptc::smem_u32(bars);
-    enum { IN_FULL = 0, IN_EMPTY = 1, OP_FULL = 2, OP_EMPTY = 3, ACC_FULL = 4, ACC_EMPTY = 5 };
-#define BAR(kind, s) (bar0 + 8u * (uint32_t)(2 * (kind) + (s)))
+#define INF(s) (bar0 + 8u * (uint32_t)(s))
+#define INE(s) (bar0 + 32u + 8u * (uint32_t)(s))
+#define OPF(s) (bar0 + 64u + 8u * (uint32_t)(s))
+#define ACCF(s) (bar0 + 96u + 8u * (uint32_t)(s))
+#define ACCE(s) (bar0 + 128u + 8u * (uint32_t)(s))
 
     // ---- one-time setup ----
-    if (warp == 0) wptc::tmem_alloc(wptc::smem_u32(tmem_slot), 256);
+    if (warp == 0) wptc::tmem_alloc(wptc::smem_u32(tmem_slot), 128 * FT_NA);
     if (tid == 32) {
-        for (int s = 0; s < 2; ++s) {
-            wptc::mbar_init(BAR(IN_FULL, s), 1);
-            wptc::mbar_init(BAR(IN_EMPTY, s), 1);
-            wptc::mbar_init(BAR(OP_FULL, s), 1);
-            wptc::mbar_init(BAR(OP_EMPTY, s), 1);
-            wptc::mbar_init(BAR(ACC_FULL, s), 1);
-            wptc::mbar_init(BAR(ACC_EMPTY, s), kEpi);
+        for (int s = 0; s < a.nin; ++s) {
+            wptc::mbar_init(INF(s), 1);
+            wptc::mbar_init(INE(s), 1);
+            wptc::mbar_init(OPF(s), 1);
+        }
+        for (int s = 0; s < FT_NA; ++s) {
+            wptc::mbar_init(ACCF(s), 1);
+            wptc::mbar_init(ACCE(s), kEpi);
         }
         wptc::mbar_fence_init();
     }
@@ -138,6 +224,12 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
     __syncthreads();
     wptc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
+#if FT_PDL
+    // programmatic dependent launch: everything above (barriers, TMEM, the plan's B
+    // image) overlapped the previous kernel's tail; the signal is read only after it
+    // has completed and its writes are visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     const long long first = blockIdx.x, stride = gridDim.x;
     const int ntiles = first < a.total_tiles ? (int)((a.total_tiles - 1 - first) / stride + 1) : 0;
 
@@ -145,46 +237,77 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
         // ================= bulk-copy producer =================
         if (lane == 0) {
             for (int i = 0; i < ntiles; ++i) {
-                const int s = a.nin > 1 ? (i & 1) : 0;
-                const uint32_t par = (uint32_t)((a.nin > 1 ? (i >> 1) : i) & 1);
-                wptc::mbar_wait(BAR(IN_EMPTY, s), par ^ 1u);
+                const int s = i % a.nin;
+                const uint32_t par = (uint32_t)((i / a.nin) & 1);
+                wptc::mbar_wait(INE(s), par ^ 1u);
                 const Geo g = geo(a, first + (long long)i * stride);
                 const uint32_t bytes = (uint32_t)(4 * (g.hi - g.lo));
-                unsigned char *dstb = s ? inbuf1 : inbuf0;
-                if (bytes > 0) {
-                    mbar_arrive_tx(BAR(IN_FULL, s), bytes);
+                FTTR(i, 0);
+                unsigned char *dstb = smem + (uint32_t)s * slotBytes;
+                if (bytes > 0 && !FT_UB_NOLOAD) {
+                    mbar_arrive_tx(INF(s), bytes);
                     const float *src = a.x + g.c * a.ldx + g.lo;
-                    bulk_g2s(wptc::smem_u32(dstb) + 4u * (uint32_t)(g.lo - g.start), src, bytes, BAR(IN_FULL, s));
+                    bulk_g2s(wptc::smem_u32(dstb) + 4u * (uint32_t)(g.lo - g.start), src, bytes, INF(s));
                 } else {
-                    mbar_arrive(BAR(IN_FULL, s));
+                    mbar_arrive(INF(s));
                 }
             }
+#if FT_PDL
+            asm volatile("griddepcontrol.launch_dependents;");  // all of this CTA's reads are issued
+#endif
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (lane == 0) {
             const uint32_t idesc = wptc::idesc_f16(128, 64), idesc2 = wptc::idesc_f16(128, 128);
-            const uint32_t op0 = wptc::smem_u32(op), b0 = wptc::smem_u32(bimg);
+            const uint32_t op0 = wptc::smem_u32(smem), b0 = wptc::smem_u32(bimg);
             for (int i = 0; i < ntiles; ++i) {
-                const int s = i & 1;
-                const uint32_t par = (uint32_t)((i >> 1) & 1);
-                wptc::mbar_wait(BAR(OP_FULL, s), par);
-                wptc::mbar_wait(BAR(ACC_EMPTY, s), par ^ 1u);
+                const int s = i % a.nin;
+                const uint32_t par = (uint32_t)((i / a.nin) & 1);
+                const int sa = i % FT_NA;
+                wptc::mbar_wait(OPF(s), par);
+                wptc::mbar_wait(ACCE(sa), (uint32_t)((i / FT_NA) & 1) ^ 1u);
                 wptc::fence_after_sync();
-                const uint32_t dm = tmem + 128u * s, dc = dm + 64u;
-                const uint32_t ahi = op0 + (2u * s) * opBytes, alo = ahi + opBytes;
+                FTTR(i, 5);
+                const uint32_t dm = tmem + 128u * sa, dc = dm + 64u;
+                const uint32_t ahi = op0 + (uint32_t)s * slotBytes, alo = ahi + opBytes;
                 const uint64_t ah0 = desc_sw128(ahi), al0 = desc_sw128(alo);
 #pragma unroll 1
-                for (int kk = 0; kk < nk; ++kk) {
+#if FT_MMA_ORDER == 1
+                for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
+                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
+                    wptc::mma_f16(dm, ah0 + 2u * kk, bb, idesc2, kk > 0);
+                }
+#pragma unroll 1
+                for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
+                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
+                    wptc::mma_f16(dc, al0 + 2u * kk, bb, idesc, 1u);
+                }
+#else
+                for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
                     const uint64_t ka = 2u * kk;  // +32 B per K step (units of 16 B)
                     // B image [atom][hi rows | lo rows x 2^11]: one N = 128 MMA puts
                     // hi.hi into columns [0, 64) and hi.lo into [64, 128) = dc
+#if FT_UB_ALIGN
+                    const uint64_t bb = desc_sw128(b0 + (FT_UB_ALIGN == 2 ? 0u : 16384u * (kk >> 2)) + 32u * (kk & 3));
+                    const uint64_t kx = 2u * (kk & 3);  // upper bound: A start stays in the first 128-B row
+                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, ah0 + kx, bb, idesc2, kk > 0);
+                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, al0 + kx, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
+#elif FT_BOFF
                     const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
-                    wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
-                    wptc::mma_f16(dc, al0 + ka, bb, idesc, 1u);
+                    const uint64_t bo = (uint64_t)(((2u * kk) >> 3) & 7u) << 49;  // matrix base offset
+                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, (ah0 + ka) | bo, bb, idesc2, kk > 0);
+                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, (al0 + ka) | bo, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
+#else
+                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
+                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
+                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, al0 + ka, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
+#endif
                 }
-                wptc::mma_commit(BAR(OP_EMPTY, s));
-                wptc::mma_commit(BAR(ACC_FULL, s));
+#endif
+                wptc::mma_commit(INE(s));  // the slot is free for the next window
+                wptc::mma_commit(ACCF(sa));
+                FTTR(i, 6);
             }
         }
     } else if (warp < 10) {
@@ -193,55 +316,49 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
         const int cw = ct >> 5;   // converter warp 0..7
         const int nq = a.W / 4;
         for (int i = 0; i < ntiles; ++i) {
-            const int s = i & 1;
-            const uint32_t par = (uint32_t)((i >> 1) & 1);
-            const int si = a.nin > 1 ? s : 0;  // fp32 window buffer
-            const uint32_t pari = (uint32_t)((a.nin > 1 ? (i >> 1) : i) & 1);
+            const int si = i % a.nin;  // slot
+            const uint32_t pari = (uint32_t)((i / a.nin) & 1);
             const Geo g = geo(a, first + (long long)i * stride);
-            const float *xr = a.x + g.c * a.ldx;
-            wptc::mbar_wait(BAR(IN_FULL, si), pari);
-            const float4 *in4 = reinterpret_cast<const float4 *>(si ? inbuf1 : inbuf0);
+            wptc::mbar_wait(INF(si), pari);
+            if (ct == 0) FTTR(i, 1);
+            float4 *in4 = reinterpret_cast<float4 *>(smem + (uint32_t)si * slotBytes);
+            if (!(g.start >= g.lo && g.start + a.W <= g.hi)) {
+                fill_window(reinterpret_cast<float *>(in4), a.x + g.c * a.ldx, g.start, g.lo, g.hi, a.N, a.W, ct);
+                named_sync(1, kConv);
+            }
             float4 v[kMaxQ];
             float m = 0.f;
-            const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
 #pragma unroll
             for (int j = 0; j < kMaxQ; ++j) {
                 const int q = ct + j * kConv;
-                if (q < nq) {
-                    const long long p0 = g.start + 4LL * q;
-                    if (interior || (p0 >= g.lo && p0 + 4 <= g.hi)) {
-                        v[j] = in4[q];
-                    } else {
-                        v[j].x = (p0 + 0 >= 0 && p0 + 0 < a.N) ? __ldg(xr + p0 + 0) : 0.f;
-                        v[j].y = (p0 + 1 >= 0 && p0 + 1 < a.N) ? __ldg(xr + p0 + 1) : 0.f;
-                        v[j].z = (p0 + 2 >= 0 && p0 + 2 < a.N) ? __ldg(xr + p0 + 2) : 0.f;
-                        v[j].w = (p0 + 3 >= 0 && p0 + 3 < a.N) ? __ldg(xr + p0 + 3) : 0.f;
-                    }
-                    if (a.pre_gain != 1.f) {
-                        v[j].x *= a.pre_gain; v[j].y *= a.pre_gain; v[j].z *= a.pre_gain; v[j].w *= a.pre_gain;
-                    }
+                if (q < nq && !FT_UB_NOCONV) {
+                    v[j] = in4[q];
                     m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
                 }
             }
             const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
             if (lane == 0) red[cw] = __uint_as_float(mb);
-            named_sync(1, kConv);
-            if (ct == 0) mbar_arrive(BAR(IN_EMPTY, si));  // window si is in registers: free it
+            named_sync(1, kConv);  // the whole window is in registers: the slot may be overwritten
+            if (ct == 0) FTTR(i, 2);
             float tmax = red[0];
 #pragma unroll
             for (int w = 1; w < 8; ++w) tmax = fmaxf(tmax, red[w]);
+            // the pre-gain folds into the power-of-two scale: max|g x| = fl(|g| max|x|) and
+            // fl(x (g sc)) = fl(g x) sc, so this equals scaling the gained window
+            tmax *= fabsf(a.pre_gain);
             int ex = 0;
             if (tmax > 0.f) frexpf(tmax, &ex);
             const float sc = ldexpf(1.f, tmax > 0.f ? 14 - ex : 0);
-            if (ct == 0) scl[s] = sc;
-            wptc::mbar_wait(BAR(OP_EMPTY, s), par ^ 1u);
-            unsigned char *ohi = op + (2 * s) * opBytes, *olo = ohi + opBytes;
+            if (ct == 0) scl[i % nscl] = sc;
+            const float scg = sc * a.pre_gain;
+            if (ct == 0) FTTR(i, 3);
+            unsigned char *ohi = smem + (uint32_t)si * slotBytes, *olo = ohi + opBytes;
 #pragma unroll
             for (int j = 0; j < kMaxQ; ++j) {
                 const int q = ct + j * kConv;
-                if (q < nq) {
-                    const float2 f01 = make_float2(v[j].x * sc, v[j].y * sc);
-                    const float2 f23 = make_float2(v[j].z * sc, v[j].w * sc);
+                if (q < nq && !FT_UB_NOCONV) {
+                    const float2 f01 = make_float2(v[j].x * scg, v[j].y * scg);
+                    const float2 f23 = make_float2(v[j].z * scg, v[j].w * scg);
                     const __half2 h01 = __float22half2_rn(f01), h23 = __float22half2_rn(f23);
                     const float2 b01 = __half22float2(h01), b23 = __half22float2(h23);
                     const __half2 l01 = __floats2half2_rn((f01.x - b01.x) * 2048.f, (f01.y - b01.y) * 2048.f);
@@ -258,7 +375,10 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
             }
             wptc::fence_proxy_async_smem();
             named_sync(1, kConv);
-            if (ct == 0) mbar_arrive(BAR(OP_FULL, s));
+            if (ct == 0) {
+                mbar_arrive(OPF(si));
+                FTTR(i, 4);
+            }
         }
     } else {
         // ================= epilogue (warps 10..13) =================
@@ -266,12 +386,13 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const int row = 32 * quarter + lane;
         for (int j = 0; j < ntiles; ++j) {
-            const int s = j & 1;
-            const uint32_t par = (uint32_t)((j >> 1) & 1);
+            const int s = j % FT_NA;
+            const uint32_t par = (uint32_t)((j / FT_NA) & 1);
             const Geo g = geo(a, first + (long long)j * stride);
-            wptc::mbar_wait(BAR(ACC_FULL, s), par);
+            wptc::mbar_wait(ACCF(s), par);
             wptc::fence_after_sync();
-            const float osc = a.out_scale / scl[s];
+            if (et == 0) FTTR(j, 7);
+            const float osc = a.out_scale / scl[j % nscl];
             const uint32_t tbase = tmem + 128u * s + ((uint32_t)(32 * quarter) << 16);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -286,11 +407,12 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
                 for (int c = 0; c < 4; ++c) {
                     float o[8];
 #pragma unroll
-                    for (int p = 0; p < 8; ++p) {
-                        o[p] = fmaf(cr[c][p], 1.f / 2048.f, mn[c][p]) * osc;
+                    for (int p = 0; p < 8; ++p) o[p] = fmaf(cr[c][p], 1.f / 2048.f, mn[c][p]) * osc;
+#pragma unroll 1
+                    for (int t = 0; t < a.n_post; ++t) {  // trailing gains, in order
+                        const float gp = a.post[t];
 #pragma unroll
-                        for (int t = 0; t < MAXPOST; ++t)
-                            if (t < a.n_post) o[p] *= a.post[t];
+                        for (int p = 0; p < 8; ++p) o[p] *= gp;
                     }
                     float4 *dst = reinterpret_cast<float4 *>(stg + row * kStagePitch + 4 * (32 * h + 8 * c));
                     dst[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -298,33 +420,39 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
                 }
             }
             wptc::fence_before_sync();
-            mbar_arrive(BAR(ACC_EMPTY, s));  // this thread's TMEM reads are done
+            mbar_arrive(ACCE(s));  // this thread's TMEM reads are done
+            if (et == 0) FTTR(j, 8);
             named_sync(2, kEpi);
             // coalesced copy-out of the 128 x 64 tile (contiguous outputs)
             float *yr = a.y + g.c * a.ldy + g.n0;
             const long long left = a.N - g.n0;
+            if (a.vec_y && left >= TC_TOUT) {
 #pragma unroll 4
-            for (int q = et; q < TC_TOUT / 4; q += kEpi) {
-                const int r = q >> 4, c4 = q & 15;
-                const float4 v = *reinterpret_cast<const float4 *>(stg + r * kStagePitch + 16 * c4);
-                const long long p0 = 4LL * q;
-                if (a.vec_y && p0 + 4 <= left) {
-                    __stcs(reinterpret_cast<float4 *>(yr + p0), v);
-                } else {
-                    if (p0 + 0 < left) yr[p0 + 0] = v.x;
-                    if (p0 + 1 < left) yr[p0 + 1] = v.y;
-                    if (p0 + 2 < left) yr[p0 + 2] = v.z;
-                    if (p0 + 3 < left) yr[p0 + 3] = v.w;
+                for (int q = et; q < TC_TOUT / 4; q += kEpi) {
+                    const int r = q >> 4, c4 = q & 15;
+                    const float4 v = *reinterpret_cast<const float4 *>(stg + r * kStagePitch + 16 * c4);
+                    if (FT_UB_NOSTORE) {
+                        if (v.x == 12345.f) yr[4 * q] = v.y;  // keeps the staging reads alive
+                    } else {
+                        __stcs(reinterpret_cast<float4 *>(yr + 4 * q), v);
+                    }
                 }
+            } else {
+                store_partial(stg, yr, left, et);
             }
             named_sync(2, kEpi);  // staging consumed before the next tile writes it
+            if (et == 0) FTTR(j, 9);
         }
     }
-#undef BAR
+#undef INF
+#undef INE
+#undef OPF
+#undef ACCF
+#undef ACCE
     wptc::fence_before_sync();
     __syncthreads();
     wptc::fence_after_sync();
-    if (warp == 0) wptc::tmem_dealloc(tmem, 256);
+    if (warp == 0) wptc::tmem_dealloc(tmem, 128 * FT_NA);
 }
 
 }  // namespace wpk
@@ -333,22 +461,38 @@ namespace wp {
 
 size_t fir_tc_smem_bytes(int W, int K, int nin) {
     const size_t opB = ((size_t)W * 2 + 1023) & ~size_t(1023);
-    const size_t inB = ((size_t)W * 4 + 1023) & ~size_t(1023);
     const size_t stgB = ((size_t)128 * wpk::kStagePitch + 1023) & ~size_t(1023);
     const size_t bB = (size_t)((K + 63) / 64) * 8192;
-    return (size_t)nin * inB + stgB + 4 * opB + 2 * bB + 12 * 8 + 64 + 1024;  // +1 KB alignment slack
+    return (size_t)nin * 2 * opB + stgB + 2 * bB + 20 * 8 + 128 + 1024;  // +1 KB alignment slack
 }
 
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(wpk::fir_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;  // the smem attribute is set at plan build (fir_tc_occupancy)
+#if FT_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(wpk::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, wpk::fir_tc_kernel, a);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+#else
     wpk::fir_tc_kernel<<<grid, wpk::kThreads, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();
+#endif
 }
 
 int fir_tc_occupancy(size_t smem) {
-    if (cudaFuncSetAttribute(wpk::fir_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    // the attribute is per kernel, shared by every plan: set the maximum once per plan build
+    if (smem > 227 * 1024 ||
+        cudaFuncSetAttribute(wpk::fir_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
         return 0;
     return smem <= 227 * 1024 ? 1 : 0;  // persistent: one CTA per SM (256 TMEM columns)
 }

@@ -21,15 +21,17 @@ struct FirTcArgs {
     long long C, N, ldx, ldy;
     long long total_tiles;
     int Tp, K, W;
-    int nin;                    // fp32 window buffers (2, or 1 for long taps)
+    int nin;                    // window/operand slots in the ring (1..4)
     const unsigned char *Bimg;  // [2][K/16][512]
     float out_scale;            // 2^-f of the taps
     float pre_gain;
     int n_post;
     float post[MAXPOST];
-    unsigned int *counter;
     int vec_x, vec_y;
+    unsigned long long *trace;  // [tiles][FT_TRACE_EV] stage stamps (-DFT_TRACE builds only)
 };
+
+constexpr int FT_TRACE_EV = 16;
 
 constexpr int FFT_M = 16384;      // complex FFT size of the overlap-save path
 constexpr int FFT_THREADS = 512;
@@ -83,6 +85,7 @@ cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long lon
 
 // tensor-core FIR (wp_fir_tc.cu)
 size_t fir_tc_smem_bytes(int W, int K, int nin);
+cudaError_t fft_ols_prepare();
 cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
 int fir_tc_occupancy(size_t smem);
 
