@@ -96,6 +96,21 @@ __device__ __forceinline__ Win win(long long tile, long long C, long long N, int
     return g;
 }
 
+// Edge tile (signal start/end, an unaligned channel, or the non-vector tail): complete
+// a window of W fp32 samples starting at sample `start` in place - zeros outside
+// [0, N), samples the bulk copy did not cover ([lo, hi)) read from global - so the
+// converters' register loads need no per-element bounds. Out of line and called
+// before the window is register-resident: rare, and off the instruction cache's hot path.
+static __device__ __noinline__ void fill_window(float *win, const float *xr, long long start, long long lo,
+                                                long long hi, long long N, int W, int t, int nthreads) {
+    for (int k = t; k < W; k += nthreads) {
+        const long long p = start + k;
+        if (p >= lo && p < hi) continue;  // bulk-copied
+        win[k] = (p >= 0 && p < N) ? __ldg(xr + p) : 0.f;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the next bulk copy overwrites it
+}
+
 }  // namespace c3d
 
 }  // namespace wpk

@@ -30,6 +30,7 @@
 //   columns), one padded output staging tile.
 #include <cuda_fp16.h>
 
+#include "wp_common.cuh"
 #include "wp_internal.h"
 #include "wp_tc.cuh"
 
@@ -140,19 +141,6 @@ __device__ __forceinline__ Geo geo(const FirTcArgs &a, long long tile) {
     if (hi > nv) hi = nv;
     g.hi = hi > g.lo ? hi : g.lo;
     return g;
-}
-
-// Edge tile (signal start/end, or an unaligned channel): complete the fp32 window in
-// place - zeros outside [0, N), samples the bulk copy did not cover read from global -
-// so the converters' hot loop has no per-element bounds (out of line: rare, and kept
-// out of the instruction cache's way).
-__device__ __noinline__ void fill_window(float *win, const float *xr, long long start, long long lo, long long hi,
-                                         long long N, int W, int ct) {
-    for (int k = ct; k < W; k += kConv) {
-        const long long p = start + k;
-        if (p >= lo && p < hi) continue;  // bulk-copied
-        win[k] = (p >= 0 && p < N) ? __ldg(xr + p) : 0.f;
-    }
 }
 
 // Last tile of a channel, or an unaligned output: guarded scalar copy-out of the staging tile.
@@ -323,7 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
             if (ct == 0) FTTR(i, 1);
             float4 *in4 = reinterpret_cast<float4 *>(smem + (uint32_t)si * slotBytes);
             if (!(g.start >= g.lo && g.start + a.W <= g.hi)) {
-                fill_window(reinterpret_cast<float *>(in4), a.x + g.c * a.ldx, g.start, g.lo, g.hi, a.N, a.W, ct);
+                c3d::fill_window(reinterpret_cast<float *>(in4), a.x + g.c * a.ldx, g.start, g.lo, g.hi, a.N, a.W, ct,
+                                 kConv);
                 named_sync(1, kConv);
             }
             float4 v[kMaxQ];

@@ -446,37 +446,18 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             const int s = i % NOP;
             const uint32_t par = (uint32_t)((i / NOP) & 1);
             const c3d::Win g = c3d::win(first + (long long)i * stride, a.C, a.N, a.H, a.W, a.vec_x);
-            const float *xr = a.x + g.c * a.ldx;
-            const bool interior = g.start >= g.lo && g.start + a.W <= g.hi;
             wptc::mbar_wait_sleep<256>(RWF, (uint32_t)(i & 1));
             if (ct == 0) LBTR(first + (long long)i * stride, 0);
+            if (!(g.start >= g.lo && g.start + a.W <= g.hi)) {
+                c3d::fill_window(reinterpret_cast<float *>(smem + lay.raw), a.x + g.c * a.ldx, g.start, g.lo, g.hi, a.N,
+                                 a.W, ct, LB_CONV);
+                ctd::named_sync(1, LB_CONV);
+            }
             float4 v[LB_QMAX];
             float m = 0.f;
-            if (interior) {
 #pragma unroll
-                for (int j = 0; j < LB_QMAX; ++j)
-                    v[j] = (ct + j * LB_CONV < nq) ? raw4[ct + j * LB_CONV] : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-#pragma unroll 1
-                for (int j = 0; j < LB_QMAX; ++j) {
-                    const int q = ct + j * LB_CONV;
-                    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (q < nq) {
-                        const long long p0 = g.start + 4LL * q;
-                        if (p0 >= g.lo && p0 + 4 <= g.hi) {
-                            t = raw4[q];
-                        } else {
-                            t.x = (p0 + 0 >= 0 && p0 + 0 < a.N) ? __ldg(xr + p0 + 0) : 0.f;
-                            t.y = (p0 + 1 >= 0 && p0 + 1 < a.N) ? __ldg(xr + p0 + 1) : 0.f;
-                            t.z = (p0 + 2 >= 0 && p0 + 2 < a.N) ? __ldg(xr + p0 + 2) : 0.f;
-                            t.w = (p0 + 3 >= 0 && p0 + 3 < a.N) ? __ldg(xr + p0 + 3) : 0.f;
-                        }
-                    }
-#pragma unroll
-                    for (int jj = 0; jj < LB_QMAX; ++jj)
-                        if (jj == j) v[jj] = t;
-                }
-            }
+            for (int j = 0; j < LB_QMAX; ++j)
+                v[j] = (ct + j * LB_CONV < nq) ? raw4[ct + j * LB_CONV] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int j = 0; j < LB_QMAX; ++j)
                 m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
