@@ -289,6 +289,41 @@ __device__ __forceinline__ void add_mlane(float (&s)[D], float (&V)[D], const fl
         for (int d = 0; d < D; ++d) s[d] += V[d];
     }
 }
+// Warp reduce-scatter of D values (padded to a power of two DP): recursive halving
+// over lane bits 4, 3, ... then an all-reduce over the remaining bits. Returns this
+// lane's total for index idx (out); lanes whose remaining low bits are zero own it.
+// DP + 5 - log2(DP) shuffles instead of 5 D for a butterfly all-reduce.
+template <int D>
+__device__ __forceinline__ float reduce_scatter(const float (&w)[D], int lane, int &idx, bool &owner) {
+    constexpr int DP = D <= 2 ? 2 : D <= 4 ? 4 : D <= 8 ? 8 : 16;
+    float cur[DP];
+#pragma unroll
+    for (int d = 0; d < DP; ++d) cur[d] = d < D ? w[d] : 0.f;
+    int id = 0;
+    int low = 0;  // lane bits reduced by all-reduce rounds
+#pragma unroll
+    for (int r = 0, off = 16, n = DP; r < 5; ++r, off >>= 1) {
+        if (n > 1) {
+            const int h = n / 2;
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int k = 0; k < h; ++k) {
+                const float send = up ? cur[k] : cur[k + h];
+                const float keep = up ? cur[k + h] : cur[k];
+                cur[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+            id = 2 * id + (up ? 1 : 0);
+            n = h;
+        } else {
+            cur[0] += __shfl_xor_sync(0xffffffffu, cur[0], off);
+            low |= off;
+        }
+    }
+    idx = id;
+    owner = (lane & low) == 0 && id < D;
+    return cur[0];
+}
+
 }  // namespace lbd
 
 template <int D, int NOP>
@@ -533,17 +568,20 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                     w[r] = acc;
                 }
             }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-                for (int d = 0; d < D; ++d) w[d] += __shfl_xor_sync(0xffffffffu, w[d], off);
+            {
+                int di;
+                bool own;
+                const float tot = lbd::reduce_scatter<D>(w, lane, di, own);
+                if (own) cb[sc4 * D + di] = tot;
+                __syncwarp();
+            }
             if (lane == 0) {
-#pragma unroll
-                for (int d = 0; d < D; ++d) cb[sc4 * D + d] = w[d];
                 ctd::arrive(CRD(sc4));
                 LBTR(tile, 5);
             }
             if ((k & (LB_BLK - 1)) == LB_BLK - 1 && lane == 0) {
+#pragma unroll
+                for (int d = 0; d < D; ++d) w[d] = cb[sc4 * D + d];
                 // block end: incl = MT c_k + agg(k) for the next block's tiles
                 float inc[D];
                 lbd::wait_words<D>(a.aggw + tile * D, inc);
