@@ -91,3 +91,21 @@ for r in rows[2:]:
     wf[role] += w
     wfi[role] += wi
 print("smem wavefronts (LSU) per role: " + ", ".join(f"{k} {v} (ideal {wfi[k]})" for k, v in wf.most_common()))
+
+# optional: the hottest source lines of one role by executed warp-instructions (NCU_ROLE_LINES=conv)
+want = __import__("os").environ.get("NCU_ROLE_LINES")
+if want:
+    per_line = collections.Counter()
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        ln = off2line.get(int(d["Address"], 16) - base)
+        role = "prologue"
+        if ln is not None:
+            for n, l0 in roles:
+                if ln >= l0:
+                    role = n
+        if role == want:
+            per_line[ln] += int(d["Instructions Executed"] or 0)
+    srcpath = [p for p in sys.argv if p.endswith(srcname)]
+    for ln, c in per_line.most_common(12):
+        print(f"  line {ln}: {c} warp-instr")
