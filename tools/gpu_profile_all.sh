@@ -9,7 +9,7 @@ prof() {  # cfg reps kernel-regex skip
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$3" -s $4 -c 1 -o gpurun_out/prof_$1 -f python tools/run_config.py $1 $2 > gpurun_out/ncu_$1.log 2>&1
   tail -1 gpurun_out/ncu_$1.log
 }
-prof cfg1 4 fused 2
+prof cfg1 4 chain_lb 2
 prof cfg2 4 fir_tc 2
 prof cfg3 4 chain_lb 2
 prof cfg5 3 chain_lb 1
