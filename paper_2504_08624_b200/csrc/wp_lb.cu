@@ -512,12 +512,40 @@ size_t lb_workspace_bytes(const LbPlan &p, long long C, long long tiles) { retur
 
 namespace {
 template <int D>
-cudaError_t launch_d(int nop, const wpk::LbArgs &a, int grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_d(int nop, const wpk::LbArgs &a, const CUtensorMap &ymap, int grid, size_t smem, cudaStream_t st) {
     if (nop == 3)
-        wpk::chain_lb_kernel<D, 3><<<grid, wpk::LB_THREADS, smem, st>>>(a);
+        wpk::chain_lb_kernel<D, 3><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
     else
-        wpk::chain_lb_kernel<D, 2><<<grid, wpk::LB_THREADS, smem, st>>>(a);
+        wpk::chain_lb_kernel<D, 2><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
     return cudaGetLastError();
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// y viewed as [C][N / 64][64] floats; boxes of 32 rows x 32 columns, 128-B swizzle
+bool encode_ymap(CUtensorMap &m, float *y, long long C, long long N, long long ldy) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc || N < 64 || C >= (1LL << 31)) return false;
+    const cuuint64_t dims[3] = {64, (cuuint64_t)(N / 64), (cuuint64_t)C};
+    const cuuint64_t strides[2] = {256, (cuuint64_t)ldy * 4};
+    const cuuint32_t box[3] = {32, 32, 1}, elem[3] = {1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
 
@@ -549,18 +577,21 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     a.vec_x = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
     a.vec_y = (ldy % 4 == 0) && (reinterpret_cast<uintptr_t>(y) % 16 == 0);
     a.trace = trace;
+    CUtensorMap ymap;
+    std::memset(&ymap, 0, sizeof ymap);
+    a.tma_y = LB_TMA_Y && a.vec_y && encode_ymap(ymap, y, C, N, ldy) ? 1 : 0;
     cudaError_t e = cudaMemsetAsync(ws, 0, 8 * lb_words(p, C, tiles), st);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(tiles, sm_count());
     switch (p.D) {
-        case 2: e = launch_d<2>(p.nop, a, grid, p.smem, st); break;
-        case 4: e = launch_d<4>(p.nop, a, grid, p.smem, st); break;
-        case 6: e = launch_d<6>(p.nop, a, grid, p.smem, st); break;
-        case 8: e = launch_d<8>(p.nop, a, grid, p.smem, st); break;
-        case 10: e = launch_d<10>(p.nop, a, grid, p.smem, st); break;
-        case 12: e = launch_d<12>(p.nop, a, grid, p.smem, st); break;
-        case 14: e = launch_d<14>(p.nop, a, grid, p.smem, st); break;
-        case 16: e = launch_d<16>(p.nop, a, grid, p.smem, st); break;
+        case 2: e = launch_d<2>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 4: e = launch_d<4>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 6: e = launch_d<6>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 8: e = launch_d<8>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 10: e = launch_d<10>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 12: e = launch_d<12>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 14: e = launch_d<14>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 16: e = launch_d<16>(p.nop, a, ymap, grid, p.smem, st); break;
         default: return cudaErrorInvalidValue;
     }
     count_launch();

@@ -57,6 +57,7 @@
 //                scale + E s_m -> padded staging -> coalesced stores
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -65,6 +66,9 @@
 
 namespace wpk {
 
+#ifndef LB_TMA_Y
+#define LB_TMA_Y 1  // epilogue: full tiles leave through TMA tensor stores from swizzled staging
+#endif
 #ifndef LB_GL_MAXD
 #define LB_GL_MAXD 16  // lane-minor M^l table for every state size (8: only up to 4 sections)
 #endif
@@ -98,6 +102,7 @@ struct LbArgs {
     unsigned long long *aggw;    // [tiles][D] {value, 1}: zero-carry tile aggregates (zeroed before the launch)
     unsigned long long *inclw;   // [blocks][C][D] {value, 1}: state after block-end tiles (k % 32 == 31)
     int vec_x, vec_y;
+    int tma_y;  // the y tensor map is valid (aligned output, N >= 64): full tiles use TMA stores
     unsigned long long *trace;   // optional: [tiles][LB_TRACE_EV] globaltimer stamps
 };
 
@@ -130,8 +135,9 @@ struct LbLayout {
         const uint32_t rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         tabs = raw + rawBytes;
         ring = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [NL][D][128] row prefixes
-        stg = ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS);  // [4 warps][32 rows] staging
-        misc = stg + 4u * 32u * CT_STG_PITCH;
+        // [4 warps][32 rows] staging, 1024-aligned (TMA SWIZZLE_128B boxes: 2 x 4 KB per warp)
+        stg = (ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS) + 1023u) & ~1023u;
+        misc = stg + (LB_TMA_Y ? 4u * 8192u : 4u * 32u * CT_STG_PITCH);  // TMA: two 4 KB boxes per warp
         // misc: Tw[2][4][D], cb[NC][D] f32; scl[RING] f32, rsc[NL] f32, red[8] f32, stag[RING] i32
         bars = (misc + 4u * (uint32_t)((8 + LB_NC) * D) + 4u * (2 * LB_RING + LB_NL + 8) + 15u) & ~15u;
         total = bars + 48 * 8 + 16 + 1024;  // + alignment slack (35 barriers + TMEM slot)
@@ -327,7 +333,7 @@ __device__ __forceinline__ float reduce_scatter(const float (&w)[D], int lane, i
 }  // namespace lbd
 
 template <int D, int NOP>
-__global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a) {
+__global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a, const __grid_constant__ CUtensorMap ymap) {
     static_assert(D >= 2 && D <= 16 && (D % 2) == 0, "2..8 sections");
     static_assert(NOP == 2 || NOP == 3, "two or three fp16 operand stages");
     static_assert(LB_NA * LB_NS <= 512, "TMEM columns");
@@ -686,7 +692,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
         const int wq = warp & 3;
         const int row = 32 * wq + lane;
         const uint32_t trow = (uint32_t)(32 * wq) << 16;
-        unsigned char *mystg = stg + (size_t)wq * 32 * CT_STG_PITCH;
+        // each warp owns its staging (TMA: 8 KB, the padded half-row path reuses it)
+        unsigned char *mystg = stg + (size_t)wq * (LB_TMA_Y ? 8192 : 32 * CT_STG_PITCH);
 #pragma unroll 1
         for (int i = 0; i < ntiles; ++i) {
             const int sa = i % LB_NA, sl = i % LB_NL, sc4 = i % LB_NC;
@@ -719,6 +726,11 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             float *yr = a.y + c * a.ldy + n0;
             const long long tleft = a.N - n0;
             const bool full = a.vec_y && tleft >= CT_TOUT;
+#if LB_TMA_Y
+            const bool tma = full && a.tma_y;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free again
+            __syncwarp();
+#endif
 #pragma unroll 1
             for (int ch = 0; ch < 4; ++ch) {
                 const int h = ch >> 1, hh = ch & 1;
@@ -740,6 +752,35 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
                         lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.x, e.y, s[2 * d2]);
                         lbd::ffma2(o16[2 * pp], o16[2 * pp + 1], e.z, e.w, s[2 * d2 + 1]);
                     }
+#if LB_TMA_Y
+                if (tma) {
+                    // this warp's 32 rows x columns [32 h, 32 h + 32) -> box h, in the 128-B swizzle
+                    // the tensor map un-swizzles (conflict-free: 8 rows hit 8 different 16-B slots)
+                    unsigned char *box = mystg + 4096 * h;
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const int j = 4 * hh + q4;
+                        *reinterpret_cast<float4 *>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                            make_float4(o16[4 * q4], o16[4 * q4 + 1], o16[4 * q4 + 2], o16[4 * q4 + 3]);
+                    }
+                    if (ch == 3) {  // one proxy fence per tile, then both boxes
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int row0 = (int)(n0 >> 6) + 32 * wq;
+#pragma unroll
+                            for (int b = 0; b < 2; ++b)
+                                asm volatile(
+                                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                        reinterpret_cast<uint64_t>(&ymap)),
+                                    "r"(wptc::smem_u32(mystg + 4096 * b)), "r"(32 * b), "r"(row0), "r"((int)c)
+                                    : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    }
+                    continue;
+                }
+#endif
                 float4 *dst = reinterpret_cast<float4 *>(mystg + lane * CT_STG_PITCH + 64 * hh);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4)
@@ -762,6 +803,9 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a)
             }
             if (row == 0) LBTR(tile, 7);
         }
+#if LB_TMA_Y
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
     }
 #undef LBTR
 #undef OPF
