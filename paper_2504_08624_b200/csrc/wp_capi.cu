@@ -949,8 +949,11 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
             a.vec_y = (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
             a.trace = (g_trace && g_trace_entries >= (size_t)a.total_tiles * wpk::FT_TRACE_EV) ? g_trace : nullptr;
             if (a.total_tiles >= (1LL << 31)) return fail(WP_EUNSUP, "more than 2^31 tiles in one call");
+            CUtensorMap ymap;
+            std::memset(&ymap, 0, sizeof ymap);
+            a.tma_y = a.vec_y && wp::encode_ymap(ymap, out, C, N, ld_out) ? 1 : 0;
             const int grid = (int)std::min<long long>(a.total_tiles, p.grid_cap);
-            e = wp::launch_fir_tc(a, grid, p.smem, stream);
+            e = wp::launch_fir_tc(a, ymap, grid, p.smem, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fir_tc launch");
         } else {
             wpk::FusedArgs a{};

@@ -76,6 +76,9 @@ constexpr int kStagePitch = 272;  // bytes per staged output row (256 + 16 pad)
 #ifndef FT_PDL
 #define FT_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail)
 #endif
+#ifndef FT_TMA
+#define FT_TMA 1  // full tiles leave through TMA tensor stores from per-warp swizzled staging
+#endif
 #ifndef FT_UB_NOLOAD
 #define FT_UB_NOLOAD 0
 #endif
@@ -158,7 +161,7 @@ __device__ __noinline__ void store_partial(const unsigned char *stg, float *yr, 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a, const __grid_constant__ CUtensorMap ymap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the operand buffers (swizzle phase = address bits)
     // align by offsetting the __shared__ array itself (keeps the shared
@@ -383,6 +386,15 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
             if (et == 0) FTTR(j, 7);
             const float osc = a.out_scale / scl[j % nscl];
             const uint32_t tbase = tmem + 128u * s + ((uint32_t)(32 * quarter) << 16);
+            const long long left = a.N - g.n0;
+            const bool tma = FT_TMA && a.tma_y && a.vec_y && left >= TC_TOUT;
+            // this warp's 32 rows as two 32 x 32 boxes (128-B swizzle), 8 KB per warp
+            unsigned char *mybox = stg + (size_t)quarter * 8192;
+            if (FT_TMA) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // boxes read
+                __syncwarp();
+                if (!tma) named_sync(2, kEpi);  // the padded tile spans every warp's boxes
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 float mn[4][8], cr[4][8];
@@ -403,18 +415,41 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
 #pragma unroll
                         for (int p = 0; p < 8; ++p) o[p] *= gp;
                     }
-                    float4 *dst = reinterpret_cast<float4 *>(stg + row * kStagePitch + 4 * (32 * h + 8 * c));
-                    dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-                    dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+                    if (FT_TMA && tma) {
+                        unsigned char *bx = mybox + 4096 * h + lane * 128;
+                        *reinterpret_cast<float4 *>(bx + (((2 * c) ^ (lane & 7)) << 4)) = make_float4(o[0], o[1], o[2], o[3]);
+                        *reinterpret_cast<float4 *>(bx + (((2 * c + 1) ^ (lane & 7)) << 4)) =
+                            make_float4(o[4], o[5], o[6], o[7]);
+                    } else {
+                        float4 *dst = reinterpret_cast<float4 *>(stg + row * kStagePitch + 4 * (32 * h + 8 * c));
+                        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+                        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+                    }
                 }
             }
             wptc::fence_before_sync();
             mbar_arrive(ACCE(s));  // this thread's TMEM reads are done
             if (et == 0) FTTR(j, 8);
+            if (FT_TMA && tma) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0 && !FT_UB_NOSTORE) {
+                    const int row0 = (int)(g.n0 >> 6) + 32 * quarter;
+#pragma unroll
+                    for (int b = 0; b < 2; ++b)
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&ymap)),
+                            "r"(wptc::smem_u32(mybox + 4096 * b)), "r"(32 * b), "r"(row0), "r"((int)g.c)
+                            : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                if (et == 0) FTTR(j, 9);
+                continue;
+            }
             named_sync(2, kEpi);
             // coalesced copy-out of the 128 x 64 tile (contiguous outputs)
             float *yr = a.y + g.c * a.ldy + g.n0;
-            const long long left = a.N - g.n0;
             if (a.vec_y && left >= TC_TOUT) {
 #pragma unroll 4
                 for (int q = et; q < TC_TOUT / 4; q += kEpi) {
@@ -432,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a) 
             named_sync(2, kEpi);  // staging consumed before the next tile writes it
             if (et == 0) FTTR(j, 9);
         }
+        if (FT_TMA && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
 #undef INF
 #undef INE
@@ -455,7 +491,7 @@ size_t fir_tc_smem_bytes(int W, int K, int nin) {
     return (size_t)nin * 2 * opB + stgB + 2 * bB + 20 * 8 + 128 + 1024;  // +1 KB alignment slack
 }
 
-cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, const CUtensorMap &ymap, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaSuccess;  // the smem attribute is set at plan build (fir_tc_occupancy)
 #if FT_PDL
     cudaLaunchConfig_t cfg = {};
@@ -468,11 +504,11 @@ cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaSt
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, wpk::fir_tc_kernel, a);
+    e = cudaLaunchKernelEx(&cfg, wpk::fir_tc_kernel, a, ymap);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 #else
-    wpk::fir_tc_kernel<<<grid, wpk::kThreads, smem, st>>>(a);
+    wpk::fir_tc_kernel<<<grid, wpk::kThreads, smem, st>>>(a, ymap);
     count_launch();
     return cudaGetLastError();
 #endif

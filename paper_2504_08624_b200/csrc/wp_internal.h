@@ -2,6 +2,7 @@
 // per-dtype kernel translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -28,6 +29,7 @@ struct FirTcArgs {
     int n_post;
     float post[MAXPOST];
     int vec_x, vec_y;
+    int tma_y;                  // the y tensor map is valid: full tiles leave through TMA stores
     unsigned long long *trace;  // [tiles][FT_TRACE_EV] stage stamps (-DFT_TRACE builds only)
 };
 
@@ -85,8 +87,11 @@ cudaError_t launch_scale_by_peak(const float *x, float *y, long long C, long lon
 
 // tensor-core FIR (wp_fir_tc.cu)
 size_t fir_tc_smem_bytes(int W, int K, int nin);
+// TMA view of an output signal y as [C][N / 64][64] floats, 32 x 32 boxes, 128-B swizzle
+// (false: no driver entry point, N < 64 or unaligned - the caller keeps its LDS/STG path)
+bool encode_ymap(CUtensorMap &m, float *y, long long C, long long N, long long ldy);
 cudaError_t fft_ols_prepare();
-cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_fir_tc(const wpk::FirTcArgs &a, const CUtensorMap &ymap, int grid, size_t smem, cudaStream_t st);
 int fir_tc_occupancy(size_t smem);
 
 // single-pass tensor-core chain with look-back (wp_lb.cu / wp_lb.cuh)

@@ -520,33 +520,6 @@ cudaError_t launch_d(int nop, const wpk::LbArgs &a, const CUtensorMap &ymap, int
     return cudaGetLastError();
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-    static EncodeTiledFn fn = [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<EncodeTiledFn>(p);
-    }();
-    return fn;
-}
-
-// y viewed as [C][N / 64][64] floats; boxes of 32 rows x 32 columns, 128-B swizzle
-bool encode_ymap(CUtensorMap &m, float *y, long long C, long long N, long long ldy) {
-    EncodeTiledFn enc = encode_tiled();
-    if (!enc || N < 64 || C >= (1LL << 31)) return false;
-    const cuuint64_t dims[3] = {64, (cuuint64_t)(N / 64), (cuuint64_t)C};
-    const cuuint64_t strides[2] = {256, (cuuint64_t)ldy * 4};
-    const cuuint32_t box[3] = {32, 32, 1}, elem[3] = {1, 1, 1};
-    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 }  // namespace
 
 cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, long long N, long long ldx, long long ldy,
@@ -598,4 +571,31 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     return e;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// y viewed as [C][N / 64][64] floats; boxes of 32 rows x 32 columns, 128-B swizzle
+bool encode_ymap(CUtensorMap &m, float *y, long long C, long long N, long long ldy) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc || N < 64 || C >= (1LL << 31)) return false;
+    const cuuint64_t dims[3] = {64, (cuuint64_t)(N / 64), (cuuint64_t)C};
+    const cuuint64_t strides[2] = {256, (cuuint64_t)ldy * 4};
+    const cuuint32_t box[3] = {32, 32, 1}, elem[3] = {1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, y, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace wp
