@@ -69,6 +69,9 @@ namespace wpk {
 #ifndef LB_TMA_Y
 #define LB_TMA_Y 1  // epilogue: full tiles leave through TMA tensor stores from swizzled staging
 #endif
+#ifndef LB_UB_NOES
+#define LB_UB_NOES 0  // upper bound (wrong output): epilogue without the E s state term
+#endif
 #ifndef LB_GL_MAXD
 #define LB_GL_MAXD 16  // lane-minor M^l table for every state size (8: only up to 4 sections)
 #endif
@@ -745,7 +748,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
 #pragma unroll
                 for (int j = 0; j < 16; ++j) o16[j] *= osc;
 #pragma unroll
-                for (int pp = 0; pp < 8; ++pp)
+                for (int pp = 0; pp < (LB_UB_NOES ? 0 : 8); ++pp)
 #pragma unroll
                     for (int d2 = 0; d2 < D / 2; ++d2) {
                         const float4 e = Ep[(8 * ch + pp) * (D / 2) + d2];
