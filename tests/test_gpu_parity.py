@@ -389,8 +389,13 @@ def test_fft_path_ragged_vs_oracle(n_taps, frames):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("pads", [(3, 5), (4, 8)], ids=["unaligned", "aligned_padded"])
 @pytest.mark.parametrize("chain_kind", ["cfg3", "fir101", "fir4096", "lp8"])
-def test_plan_execute_unaligned_strides(chain_kind):
+def test_plan_execute_unaligned_strides(chain_kind, pads):
+    """(3, 5): rows not 16-byte aligned - scalar edge paths, no TMA stores;
+    (4, 8): aligned padded rows - full tiles leave through the TMA tensor map
+    (row stride ldy), the last partial tile through the guarded path; the
+    padding must stay untouched either way."""
     import torch
 
     from paper_2504_08624_b200 import engine
@@ -403,10 +408,10 @@ def test_plan_execute_unaligned_strides(chain_kind):
         "lp8": [wp.design_butterworth("lp", 8, 2000)],
     }[chain_kind]
     bound = wp.Chain(stages).bind(fs).stages
-    C, N = 3, 30011
+    C, N = 3, 30011 if pads[0] % 4 else 30020  # aligned case: N % 4 == 0, N % 64 != 0
     rng = np.random.default_rng(17)
     x = rng.standard_normal((C, N)).astype(np.float32)
-    ldx, ldy = N + 3, N + 5  # rows not 16-byte aligned: scalar edge paths
+    ldx, ldy = N + pads[0], N + pads[1]
     xd = torch.zeros((C, ldx), dtype=torch.float32, device="cuda")
     xd[:, :N] = torch.from_numpy(x)
     yd = torch.full((C, ldy), 7.0, dtype=torch.float32, device="cuda")
