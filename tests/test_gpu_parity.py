@@ -560,6 +560,56 @@ def test_plan_execute_in_cuda_graph():
     assert oracle.parity_error(y_graph.double().cpu().numpy(), ref) <= IIR_TOL
 
 
+@pytest.mark.gpu
+def test_fir_passes_back_to_back_programmatic_launch():
+    """Two FIR-only tensor-core passes in a row (the second reads the first's
+    output) eagerly and captured in one CUDA graph, replayed with NEW input: the
+    programmatic dependent launch must still order the second kernel after the
+    first one's stores (griddepcontrol.wait before any read of the signal)."""
+    import torch
+
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    pa = engine.plan_for(wp.Chain([wp.design_fir("lp", 101, 9000)]).bind(fs).stages, device=0)
+    pb = engine.plan_for(wp.Chain([wp.design_fir("hp", 31, 300)]).bind(fs).stages, device=0)
+    assert "fir_tc" in pa.describe()[0] and "fir_tc" in pb.describe()[0]
+    C, N = 6, 1 << 20
+    rng = np.random.default_rng(21)
+    x = torch.from_numpy(rng.standard_normal((C, N)).astype(np.float32)).cuda()
+    mid = torch.empty_like(x)
+    out = torch.empty_like(x)
+    na, nb = pa.workspace_bytes(C, N), pb.workspace_bytes(C, N)
+    wsa = torch.empty(max(na, 1), dtype=torch.uint8, device="cuda")
+    wsb = torch.empty(max(nb, 1), dtype=torch.uint8, device="cuda")
+
+    def run(st):
+        pa.execute(x.data_ptr(), mid.data_ptr(), C, N, N, N, wsa.data_ptr(), na, st)
+        pb.execute(mid.data_ptr(), out.data_ptr(), C, N, N, N, wsb.data_ptr(), nb, st)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            run(s.cuda_stream)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = out.clone()
+    ref = oracle.pipe(x.double().cpu().numpy(), wp.Chain([wp.design_fir("lp", 101, 9000),
+                                                          wp.design_fir("hp", 31, 300)]).bind(fs).stages)
+    assert oracle.parity_error(eager.double().cpu().numpy(), ref) <= 2 * FIR_TOL
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run(torch.cuda.current_stream().cuda_stream)
+    x.copy_(torch.from_numpy(rng.standard_normal((C, N)).astype(np.float32)))
+    out.fill_(5.0)
+    g.replay()
+    torch.cuda.synchronize()
+    ref2 = oracle.pipe(x.double().cpu().numpy(), wp.Chain([wp.design_fir("lp", 101, 9000),
+                                                           wp.design_fir("hp", 31, 300)]).bind(fs).stages)
+    assert oracle.parity_error(out.double().cpu().numpy(), ref2) <= 2 * FIR_TOL
+
+
 # ---- LTI fuser coverage: whole runs of IIR / FIR / gain stages in one pass ----
 
 
