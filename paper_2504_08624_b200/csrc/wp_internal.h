@@ -97,6 +97,7 @@ int fir_tc_occupancy(size_t smem);
 // single-pass tensor-core chain with look-back (wp_lb.cu / wp_lb.cuh)
 struct LbPlan {
     int D = 0, H = 0, K = 0, W = 0, nop = 2;
+    bool tma_stage = false;  // epilogue staging laid out for TMA output stores
     size_t smem = 0;
     unsigned char *d_bimg = nullptr;
     float *d_stabs = nullptr, *d_MTl = nullptr;
@@ -108,7 +109,7 @@ struct LbPlan {
 };
 // S sections (<= 8) and T taps (T <= 1: no FIR) fit the kernel's shared memory
 bool lb_fits(int S, int T);
-size_t lb_smem_bytes(int D, int H, int nop);
+size_t lb_smem_bytes(int D, int H, int nop, bool tma);
 int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps, double gain,
              std::string &err);
 void lb_free(LbPlan &p);

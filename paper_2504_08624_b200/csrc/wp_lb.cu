@@ -243,15 +243,15 @@ cudaError_t set_attr_any(int D, int nop, size_t smem) {
 
 }  // namespace
 
-size_t lb_smem_bytes(int D, int H, int nop) {
-    return wpk::LbLayout(wpk::CT_TOUT + H, H + 64, D, nop).total;
+size_t lb_smem_bytes(int D, int H, int nop, bool tma) {
+    return wpk::LbLayout(wpk::CT_TOUT + H, H + 64, D, nop, tma).total;
 }
 
 bool lb_fits(int S, int T) {
     if (S < 1 || S > 8) return false;
     const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
     if (H > wpk::LB_MAX_H) return false;
-    return lb_smem_bytes(2 * S, H, 2) <= 227 * 1024;
+    return lb_smem_bytes(2 * S, H, 2, false) <= 227 * 1024;
 }
 
 void lb_free(LbPlan &p) {
@@ -484,8 +484,10 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     p.H = H;
     p.K = K;
     p.W = W;
-    p.nop = lb_smem_bytes(D, H, 3) <= 227 * 1024 ? 3 : 2;
-    p.smem = lb_smem_bytes(D, H, p.nop);
+    // TMA output staging where it fits next to two operand stages, three stages where they fit
+    p.tma_stage = LB_TMA_Y && lb_smem_bytes(D, H, 2, true) <= 227 * 1024;
+    p.nop = lb_smem_bytes(D, H, 3, p.tma_stage) <= 227 * 1024 ? 3 : 2;
+    p.smem = lb_smem_bytes(D, H, p.nop, p.tma_stage);
     // the attribute is per kernel, shared by every plan of this (D, stages) shape: set the maximum
     e = set_attr_any(D, p.nop, 227 * 1024);
     if (e != cudaSuccess) {
@@ -495,8 +497,9 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     char buf[256];
     snprintf(buf, sizeof buf,
              "chain_lb[iir=%d fir=%d gain=%g] tcgen05 f16x3 M128xN%d K=%d halo=%d tile=%d stages=%d smem=%zu "
-             "fp32 scan (balanced basis, %d/%d sections), look-back",
-             S, T > 1 ? T : 0, gain, wpk::LB_NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S);
+             "fp32 scan (balanced basis, %d/%d sections), look-back, %s out",
+             S, T > 1 ? T : 0, gain, wpk::LB_NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S,
+             p.tma_stage ? "TMA" : "LDS/STG");
     p.desc = buf;
     return WP_OK;
 }
@@ -552,7 +555,8 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     a.trace = trace;
     CUtensorMap ymap;
     std::memset(&ymap, 0, sizeof ymap);
-    a.tma_y = LB_TMA_Y && a.vec_y && encode_ymap(ymap, y, C, N, ldy) ? 1 : 0;
+    a.tma_stage = p.tma_stage ? 1 : 0;
+    a.tma_y = p.tma_stage && a.vec_y && encode_ymap(ymap, y, C, N, ldy) ? 1 : 0;
     cudaError_t e = cudaMemsetAsync(ws, 0, 8 * lb_words(p, C, tiles), st);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(tiles, sm_count());

@@ -105,7 +105,8 @@ struct LbArgs {
     unsigned long long *aggw;    // [tiles][D] {value, 1}: zero-carry tile aggregates (zeroed before the launch)
     unsigned long long *inclw;   // [blocks][C][D] {value, 1}: state after block-end tiles (k % 32 == 31)
     int vec_x, vec_y;
-    int tma_y;  // the y tensor map is valid (aligned output, N >= 64): full tiles use TMA stores
+    int tma_stage;  // the plan's layout has TMA staging (LbLayout tma)
+    int tma_y;      // and the y tensor map is valid (aligned output, N >= 64): full tiles use TMA stores
     unsigned long long *trace;   // optional: [tiles][LB_TRACE_EV] globaltimer stamps
 };
 
@@ -129,7 +130,9 @@ struct LbLayout {
     uint32_t opBytes, bBytes;
     uint32_t bimg, op, raw, tabs, ring, stg, misc, bars;
     uint32_t total;
-    __host__ __device__ LbLayout(int W, int K, int D, int nop) {
+    // tma: 8 KB of staging per epilogue warp (two 32 x 32 TMA boxes) instead of 32 padded
+    // half rows; chosen per plan only where it still fits (fusion reach is unchanged)
+    __host__ __device__ LbLayout(int W, int K, int D, int nop, bool tma) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
         bBytes = lb_bbytes(K);
         bimg = 0;
@@ -140,7 +143,7 @@ struct LbLayout {
         ring = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [NL][D][128] row prefixes
         // [4 warps][32 rows] staging, 1024-aligned (TMA SWIZZLE_128B boxes: 2 x 4 KB per warp)
         stg = (ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS) + 1023u) & ~1023u;
-        misc = stg + (LB_TMA_Y ? 4u * 8192u : 4u * 32u * CT_STG_PITCH);  // TMA: two 4 KB boxes per warp
+        misc = stg + (tma ? 4u * 8192u : 4u * 32u * CT_STG_PITCH);
         // misc: Tw[2][4][D], cb[NC][D] f32; scl[RING] f32, rsc[NL] f32, red[8] f32, stag[RING] i32
         bars = (misc + 4u * (uint32_t)((8 + LB_NC) * D) + 4u * (2 * LB_RING + LB_NL + 8) + 15u) & ~15u;
         total = bars + 48 * 8 + 16 + 1024;  // + alignment slack (35 barriers + TMEM slot)
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
     unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nk = a.K / 16;
-    const LbLayout lay(a.W, a.K, D, NOP);
+    const LbLayout lay(a.W, a.K, D, NOP, a.tma_stage != 0);
     unsigned char *bimg = smem + lay.bimg;
     unsigned char *op = smem + lay.op;
     float *tabs = reinterpret_cast<float *>(smem + lay.tabs);
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
         const int row = 32 * wq + lane;
         const uint32_t trow = (uint32_t)(32 * wq) << 16;
         // each warp owns its staging (TMA: 8 KB, the padded half-row path reuses it)
-        unsigned char *mystg = stg + (size_t)wq * (LB_TMA_Y ? 8192 : 32 * CT_STG_PITCH);
+        unsigned char *mystg = stg + (size_t)wq * (a.tma_stage ? 8192 : 32 * CT_STG_PITCH);
 #pragma unroll 1
         for (int i = 0; i < ntiles; ++i) {
             const int sa = i % LB_NA, sl = i % LB_NL, sc4 = i % LB_NC;

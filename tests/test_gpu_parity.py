@@ -732,3 +732,26 @@ def test_eight_sections_one_pass(maxs, passes, monkeypatch):
                  torch.cuda.current_stream().cuda_stream)
     ref = oracle.pipe(x.astype(np.float64), bound)
     assert oracle.parity_error(yd.cpu().numpy().astype(np.float64), ref) <= IIR_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sections,taps", [(4, 193), (5, 193), (6, 129), (7, 65), (8, 65)])
+def test_fusion_reach_unchanged_by_output_staging(sections, taps, monkeypatch):
+    """IIR + FIR passes keep their one-pass reach: the TMA output staging is laid
+    out only where it fits next to the operands (else the LDS/STG staging).
+    More than 5 sections are split by default (measured faster): WP_LB_MAXS=8
+    asks for the one-pass form the reach is about."""
+    from paper_2504_08624_b200 import engine
+
+    if sections > 5:
+        monkeypatch.setenv("WP_LB_MAXS", "8")
+    fs = 48000
+    iir = wp.design_butterworth("lp", 2 * sections, 3000 + 7 * taps)  # distinct plans (no cache hits)
+    fir = wp.design_fir("lp", taps, 9000)
+    bound = wp.Chain([iir, fir]).bind(fs).stages
+    plan = engine.plan_for(bound, device=0)
+    desc = plan.describe_for(4, 8192 * 20)
+    assert plan.num_passes == 1 and desc[0].startswith("chain_lb"), desc
+    w = wp.white_noise(0.2, 2, fs, seed=5)
+    y = wp.pipe(w, wp.Chain([iir, fir])).samples
+    assert oracle.parity_error(y, oracle.pipe(w.samples, bound)) <= IIR_TOL

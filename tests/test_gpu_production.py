@@ -155,3 +155,30 @@ def test_acceptance_random_firs(strategy):
         y = wp.apply_fir(f, w, strategy=strategy).samples
         ref = oracle.fir_direct(taps, w.samples)
         assert oracle.parity_error(y, ref) <= FIR_TOL, (case, T, C, N)
+
+
+def test_multitile_random_chains():
+    """Random IIR (1-5 sections) | FIR (8-257 taps) | gain chains and FIR-only
+    chains over 2-12 tiles of 8192 plus a random tail: one chain_lb / fir_tc pass
+    each, full tiles through the TMA output path, the last partial tile through
+    the guarded stores."""
+    rng = np.random.default_rng(0xB200)
+    fs = 48000
+    for case in range(36):
+        C = int(rng.integers(1, 10))
+        N = 8192 * int(rng.integers(2, 13)) + int(rng.integers(0, 8192))
+        T = int(rng.integers(8, 258))
+        taps = rng.uniform(-1, 1, T) / np.sqrt(T)
+        fir = wp.FirFilter.from_taps(taps, fs)
+        if case % 3 == 2:
+            stages = [fir, wp.Gain(0.7)]
+            kind = "fir_tc"
+        else:
+            stages = [random_cascade(rng, max_sections=5, fs=fs), fir, wp.Gain(1.3)]
+            kind = "chain_lb"
+        desc = wp.Chain(stages).bind(fs).stages
+        assert any(kind in d for d in engine.plan_for(desc, device=0).describe_for(C, N)), (case, kind)
+        x = rng.standard_normal((C, N))
+        y, ref = _run(stages, x, fs)
+        tol = FIR_TOL if kind == "fir_tc" else IIR_TOL
+        assert oracle.parity_error(y, ref) <= tol, (case, kind, C, N, T)
