@@ -21,13 +21,16 @@
 //
 // Pipeline (persistent, one CTA per SM, static tile schedule):
 //   warp 0   bulk-copy producer: fp32 window -> smem (cp.async.bulk, mbarrier tx)
-//   warp 1   MMA issuer (one thread): 3 x K/16 tcgen05.mma per tile
-//   warps 2-9 convert window -> swizzled fp16 hi/lo operands
-//   warps 10-13 epilogue: TMEM -> registers -> padded smem staging ->
-//            coalesced stores (runs concurrently with the next conversion)
+//   warp 1   MMA issuer (one thread): 2 x K/16 tcgen05.mma per tile
+//   warps 2-9 convert window -> swizzled fp16 hi/lo operands (in place)
+//   warps 10-13 epilogue: TMEM -> registers -> per-warp 128-B swizzled boxes ->
+//            two TMA tensor stores per warp (the last partial tile of a channel:
+//            padded staging, guarded stores); runs concurrently with the next
+//            conversion
 //   a ring of 2-4 slots (each: the fp32 window, then in place its fp16 hi | lo
 //   operands until the MMAs have read them), TMEM accumulators (2 x 128
-//   columns), one padded output staging tile.
+//   columns), one output staging area. Launched with programmatic dependent
+//   launch: the prologue overlaps the previous kernel's tail.
 #include <cuda_fp16.h>
 
 #include "wp_common.cuh"
@@ -60,18 +63,6 @@ constexpr int kStagePitch = 272;  // bytes per staged output row (256 + 16 pad)
 #define FTTR(i, ev) \
     do {            \
     } while (0)
-#endif
-#ifndef FT_MMA_ORDER
-#define FT_MMA_ORDER 0  // 1: all hi MMAs, then all lo MMAs (A/B)
-#endif
-#ifndef FT_UB_MMA
-#define FT_UB_MMA 0  // upper bound: 1 issues only the N=128 hi MMAs, 2 only the N=64 lo MMAs
-#endif
-#ifndef FT_UB_ALIGN
-#define FT_UB_ALIGN 0  // upper bound: 1 keeps every A start in the first swizzle row, 2 also B
-#endif
-#ifndef FT_BOFF
-#define FT_BOFF 0  // descriptor matrix base offset = start row within the swizzle atom (A/B)
 #endif
 #ifndef FT_PDL
 #define FT_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail)
@@ -264,38 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) fir_tc_kernel(const FirTcArgs a, 
                 const uint32_t ahi = op0 + (uint32_t)s * slotBytes, alo = ahi + opBytes;
                 const uint64_t ah0 = desc_sw128(ahi), al0 = desc_sw128(alo);
 #pragma unroll 1
-#if FT_MMA_ORDER == 1
-                for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
-                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
-                    wptc::mma_f16(dm, ah0 + 2u * kk, bb, idesc2, kk > 0);
-                }
-#pragma unroll 1
-                for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
-                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
-                    wptc::mma_f16(dc, al0 + 2u * kk, bb, idesc, 1u);
-                }
-#else
                 for (int kk = 0; kk < (FT_UB_NOMMA ? 0 : nk); ++kk) {
                     const uint64_t ka = 2u * kk;  // +32 B per K step (units of 16 B)
                     // B image [atom][hi rows | lo rows x 2^11]: one N = 128 MMA puts
                     // hi.hi into columns [0, 64) and hi.lo into [64, 128) = dc
-#if FT_UB_ALIGN
-                    const uint64_t bb = desc_sw128(b0 + (FT_UB_ALIGN == 2 ? 0u : 16384u * (kk >> 2)) + 32u * (kk & 3));
-                    const uint64_t kx = 2u * (kk & 3);  // upper bound: A start stays in the first 128-B row
-                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, ah0 + kx, bb, idesc2, kk > 0);
-                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, al0 + kx, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
-#elif FT_BOFF
                     const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
-                    const uint64_t bo = (uint64_t)(((2u * kk) >> 3) & 7u) << 49;  // matrix base offset
-                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, (ah0 + ka) | bo, bb, idesc2, kk > 0);
-                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, (al0 + ka) | bo, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
-#else
-                    const uint64_t bb = desc_sw128(b0 + 16384u * (kk >> 2) + 32u * (kk & 3));
-                    if (FT_UB_MMA != 2) wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
-                    if (FT_UB_MMA != 1) wptc::mma_f16(dc, al0 + ka, bb, idesc, FT_UB_MMA == 2 ? (kk > 0) : 1u);
-#endif
+                    wptc::mma_f16(dm, ah0 + ka, bb, idesc2, kk > 0);
+                    wptc::mma_f16(dc, al0 + ka, bb, idesc, 1u);
                 }
-#endif
                 wptc::mma_commit(INE(s));  // the slot is free for the next window
                 wptc::mma_commit(ACCF(sa));
                 FTTR(i, 6);
