@@ -674,7 +674,10 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                 }
                 if (keep.empty()) continue;
                 for (size_t idx = 0; idx < keep.size(); ++idx) {
-                    if (cur.S == lb_max_sections(run_sections[si]) || (cur.T > 0 && cur.T - 1 > lbh)) close();
+                    // ... and while the IIR + FIR pass fits the single-pass kernel's shared memory
+                    if (cur.S == lb_max_sections(run_sections[si]) || (cur.T > 0 && cur.T - 1 > lbh) ||
+                        (cur.T > 1 && !wp::lb_fits(cur.S + 1, cur.T)))
+                        close();
                     for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * keep[idx] + j]);
                     cur.S += 1;
                     cur.prec_flag |= st.flags & (WP_IIR_PREC_F32 | WP_IIR_PREC_F64);
@@ -693,6 +696,8 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                 } else if (long_fir && cur.S > 0) {
                     close();
                 }
+                if (cur.S > 0 && !wp::lb_fits(cur.S, cur.T > 0 ? cur.T + st.n - 1 : st.n))
+                    close();  // the merged pass would not fit the single-pass kernel: the FIR starts a new one
                 if (cur.T > 0) {
                     // convolve with the pass's FIR (both causal, same-length truncation later)
                     std::vector<long double> t((size_t)cur.T + st.n - 1, 0.0L);
