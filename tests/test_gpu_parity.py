@@ -755,3 +755,22 @@ def test_fusion_reach_unchanged_by_output_staging(sections, taps, monkeypatch):
     w = wp.white_noise(0.2, 2, fs, seed=5)
     y = wp.pipe(w, wp.Chain([iir, fir])).samples
     assert oracle.parity_error(y, oracle.pipe(w.samples, bound)) <= IIR_TOL
+
+
+@pytest.mark.gpu
+def test_iir_fir_iir_too_large_for_one_pass():
+    """IIR(1) | FIR(252) | IIR(4): 5 sections + a 252-tap FIR do not fit one
+    chain_lb pass; the planner closes the pass instead of handing the CUDA-core
+    fused kernel a configuration it cannot hold (found by tools/stress_random.py)."""
+    from paper_2504_08624_b200 import engine
+
+    fs = 48000
+    rng = np.random.default_rng(1971)
+    stages = [wp.design_butterworth("hp", 2, 200), wp.FirFilter.from_taps(rng.uniform(-1, 1, 252) / 16, fs),
+              wp.design_chebyshev1("lp", 8, 0.5, 9000)]
+    bound = wp.Chain(stages).bind(fs).stages
+    plan = engine.plan_for(bound, device=0)
+    assert plan.num_passes >= 2
+    w = wp.white_noise(0.5, 3, fs, seed=4)
+    y = wp.pipe(w, wp.Chain(stages)).samples
+    assert oracle.parity_error(y, oracle.pipe(w.samples, bound)) <= IIR_TOL
