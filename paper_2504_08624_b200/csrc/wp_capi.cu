@@ -631,17 +631,30 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
     const bool lti = lb_enabled();
     // IIR sections (non-identity) in the LTI run (stages up to the next Normalize) of each stage
     std::vector<int> run_sections(n_stages > 0 ? n_stages : 1, 0);
+    std::vector<char> run_one_pass(n_stages > 0 ? n_stages : 1, 0);
     for (int a = 0; a < n_stages;) {
         int b = a, tot = 0;
+        std::vector<double> run_sos;
         while (b < n_stages && stages[b].kind != WP_STAGE_NORMALIZE) {
             if (stages[b].kind == WP_STAGE_IIR && stages[b].coef)
                 for (int k = 0; k < stages[b].n; ++k) {
                     const double *r = stages[b].coef + 5 * k;
-                    if (!(r[0] == 1.0 && r[1] == 0.0 && r[2] == 0.0 && r[3] == 0.0 && r[4] == 0.0)) ++tot;
+                    if (!(r[0] == 1.0 && r[1] == 0.0 && r[2] == 0.0 && r[3] == 0.0 && r[4] == 0.0)) {
+                        ++tot;
+                        run_sos.insert(run_sos.end(), r, r + 5);
+                    }
                 }
             ++b;
         }
-        for (int q = a; q < b; ++q) run_sections[q] = tot;
+        // a run of 6-8 sections whose block basis is ill-conditioned in fp32 stays ONE
+        // pass (then in the globally balanced basis): splitting it would pass an fp32
+        // intermediate whose error later sections can amplify past the bar
+        const bool one = lti && tot > 5 && tot <= 8 && !std::getenv("WP_LB_MAXS") &&
+                         wp::lb_ill_conditioned(run_sos.data(), tot);
+        for (int q = a; q < b; ++q) {
+            run_sections[q] = tot;
+            run_one_pass[q] = one;
+        }
         a = b + 1;
     }
     for (int si = 0; si < n_stages; ++si) {
@@ -675,7 +688,8 @@ int wp_plan_create(const wp_stage *stages, int32_t n_stages, wp_plan **out_plan)
                 if (keep.empty()) continue;
                 for (size_t idx = 0; idx < keep.size(); ++idx) {
                     // ... and while the IIR + FIR pass fits the single-pass kernel's shared memory
-                    if (cur.S == lb_max_sections(run_sections[si]) || (cur.T > 0 && cur.T - 1 > lbh) ||
+                    if (cur.S == (run_one_pass[si] ? 8 : lb_max_sections(run_sections[si])) ||
+                        (cur.T > 0 && cur.T - 1 > lbh) ||
                         (cur.T > 1 && !wp::lb_fits(cur.S + 1, cur.T)))
                         close();
                     for (int j = 0; j < 5; ++j) cur.sos.push_back(st.coef[5 * keep[idx] + j]);

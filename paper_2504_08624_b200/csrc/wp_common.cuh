@@ -14,12 +14,13 @@ constexpr int CT_TOUT = CT_ROWS * 64;  // outputs per tile (rows of 64 samples)
 constexpr int CT_STG_PITCH = 144;      // epilogue staging row pitch: 32 floats + 16 B pad
 
 // block-lower-triangular row r of a D x D transfer matrix (2 x 2 section blocks,
-// cascade order) has entries q < lt_nj(r); lt_off packs the rows
-__host__ __device__ constexpr int lt_nj(int r) { return 2 * ((r >> 1) + 1); }
-__host__ __device__ constexpr int lt_off(int r) {
-    return (r & 1) ? 2 * ((r >> 1) + 1) * ((r >> 1) + 1) : 2 * (r >> 1) * ((r >> 1) + 1);
+// cascade order) has entries q < lt_nj(D, r, false); lt_off packs the rows. A
+// dense (globally balanced) basis has full rows.
+__host__ __device__ constexpr int lt_nj(int D, int r, bool dense) { return dense ? D : 2 * ((r >> 1) + 1); }
+__host__ __device__ constexpr int lt_off(int D, int r, bool dense) {
+    return dense ? r * D : ((r & 1) ? 2 * ((r >> 1) + 1) * ((r >> 1) + 1) : 2 * (r >> 1) * ((r >> 1) + 1));
 }
-__host__ __device__ constexpr int lt_size(int D) { return lt_off(D); }
+__host__ __device__ constexpr int lt_size(int D, bool dense) { return lt_off(D, D, dense); }
 
 namespace ctd {
 

@@ -98,6 +98,8 @@ int fir_tc_occupancy(size_t smem);
 struct LbPlan {
     int D = 0, H = 0, K = 0, W = 0, nop = 2;
     bool tma_stage = false;  // epilogue staging laid out for TMA output stores
+    bool dense = false;      // globally balanced (dense) state basis: the block basis is ill-conditioned
+    double cond_ratio = 0;   // fp32 roundoff gain of the block basis
     size_t smem = 0;
     unsigned char *d_bimg = nullptr;
     float *d_stabs = nullptr, *d_MTl = nullptr;
@@ -109,7 +111,8 @@ struct LbPlan {
 };
 // S sections (<= 8) and T taps (T <= 1: no FIR) fit the kernel's shared memory
 bool lb_fits(int S, int T);
-size_t lb_smem_bytes(int D, int H, int nop, bool tma);
+size_t lb_smem_bytes(int D, int H, int nop, bool tma, bool dense);
+bool lb_ill_conditioned(const double *sos, int S);  // block basis fp32 roundoff gain past the dense threshold
 int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps, double gain,
              std::string &err);
 void lb_free(LbPlan &p);

@@ -157,6 +157,117 @@ bool balance_section(const double *sec, LD T[4], LD Ti[4]) {
     return true;
 }
 
+// Globally balanced realization of (A, B, C) (dense-basis plans): T Wc T^T =
+// T^-T Wo T^-1 = diag(Hankel singular values). Wc = Lc Lc^T, N = Lc^T Wo Lc =
+// U S^2 U^T (cyclic Jacobi), T = S^1/2 U^T Lc^-1, T^-1 = Lc U S^-1/2. The state
+// matrix becomes dense; the fp32 scan is then conditioned by the whole cascade,
+// not section by section.
+MatL lyap_doubling(const MatL &A, const MatL &Q, int D);
+constexpr double kDenseRatio = 20.0;  // calibrated on 300 random 6-section cascades (tools/six_section_probe.py)
+bool global_balance(MatL &A, std::vector<LD> &B, std::vector<LD> &C, int D) {
+    MatL Qc((size_t)D * D), Qo((size_t)D * D), At((size_t)D * D);
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            Qc[i * D + j] = B[i] * B[j];
+            Qo[i * D + j] = C[i] * C[j];
+            At[i * D + j] = A[j * D + i];
+        }
+    MatL Wc = lyap_doubling(A, Qc, D);
+    const MatL Wo = lyap_doubling(At, Qo, D);
+    LD tr = 0;
+    for (int i = 0; i < D; ++i) tr += Wc[i * D + i];
+    if (!(tr > 0) || !std::isfinite((double)tr)) return false;
+    for (int i = 0; i < D; ++i) Wc[i * D + i] += 1e-15L * tr / D;
+    // Cholesky Wc = L L^T (lower)
+    MatL L((size_t)D * D, 0.0L);
+    for (int j = 0; j < D; ++j) {
+        LD v = Wc[j * D + j];
+        for (int k = 0; k < j; ++k) v -= L[j * D + k] * L[j * D + k];
+        if (!(v > 0)) return false;
+        L[j * D + j] = std::sqrt(v);
+        for (int i = j + 1; i < D; ++i) {
+            LD w = Wc[i * D + j];
+            for (int k = 0; k < j; ++k) w -= L[i * D + k] * L[j * D + k];
+            L[i * D + j] = w / L[j * D + j];
+        }
+    }
+    // Linv (lower triangular inverse)
+    MatL Li((size_t)D * D, 0.0L);
+    for (int c = 0; c < D; ++c) {
+        for (int i = 0; i < D; ++i) {
+            LD v = (i == c) ? 1.0L : 0.0L;
+            for (int k = 0; k < i; ++k) v -= L[i * D + k] * Li[k * D + c];
+            Li[i * D + c] = v / L[i * D + i];
+        }
+    }
+    // N = L^T Wo L
+    MatL LT((size_t)D * D);
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) LT[i * D + j] = L[j * D + i];
+    MatL N = mat_mul(mat_mul(LT, Wo, D), L, D);
+    // cyclic Jacobi: N = U diag(ev) U^T
+    MatL U((size_t)D * D, 0.0L);
+    for (int i = 0; i < D; ++i) U[i * D + i] = 1.0L;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        LD off = 0;
+        for (int p = 0; p < D; ++p)
+            for (int q = p + 1; q < D; ++q) off += N[p * D + q] * N[p * D + q];
+        if (off < 1e-36L) break;
+        for (int p = 0; p < D; ++p)
+            for (int q = p + 1; q < D; ++q) {
+                const LD apq = N[p * D + q];
+                if (std::fabs(apq) < 1e-300L) continue;
+                const LD theta = (N[q * D + q] - N[p * D + p]) / (2 * apq);
+                const LD t = (theta >= 0 ? 1.0L : -1.0L) / (std::fabs(theta) + std::sqrt(theta * theta + 1));
+                const LD c = 1 / std::sqrt(t * t + 1), sn = t * c;
+                for (int k = 0; k < D; ++k) {  // rotate columns p, q of N and U
+                    const LD nkp = N[k * D + p], nkq = N[k * D + q];
+                    N[k * D + p] = c * nkp - sn * nkq;
+                    N[k * D + q] = sn * nkp + c * nkq;
+                    const LD ukp = U[k * D + p], ukq = U[k * D + q];
+                    U[k * D + p] = c * ukp - sn * ukq;
+                    U[k * D + q] = sn * ukp + c * ukq;
+                }
+                for (int k = 0; k < D; ++k) {  // and rows p, q
+                    const LD npk = N[p * D + k], nqk = N[q * D + k];
+                    N[p * D + k] = c * npk - sn * nqk;
+                    N[q * D + k] = sn * npk + c * nqk;
+                }
+            }
+    }
+    LD smax = 0;
+    std::vector<LD> sg(D);
+    for (int i = 0; i < D; ++i) {
+        sg[i] = std::sqrt(std::max(N[i * D + i], 0.0L));  // Hankel singular values
+        smax = std::max(smax, sg[i]);
+    }
+    if (!(smax > 0)) return false;
+    MatL T((size_t)D * D, 0.0L), Ti((size_t)D * D, 0.0L);
+    for (int i = 0; i < D; ++i) {
+        const LD si = std::max(sg[i], 1e-12L * smax);
+        const LD a = std::sqrt(si), ai = 1 / a;
+        for (int j = 0; j < D; ++j) {
+            LD tv = 0, tiv = 0;
+            for (int k = 0; k < D; ++k) {
+                tv += U[k * D + i] * Li[k * D + j];  // (U^T Linv)[i][j]
+                tiv += L[j * D + k] * U[k * D + i];  // (L U)[j][i]
+            }
+            T[i * D + j] = a * tv;
+            Ti[j * D + i] = tiv * ai;
+        }
+    }
+    A = mat_mul(mat_mul(T, A, D), Ti, D);
+    std::vector<LD> Bn(D, 0.0L), Cn(D, 0.0L);
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            Bn[i] += T[i * D + j] * B[j];
+            Cn[j] += C[i] * Ti[i * D + j];
+        }
+    B = Bn;
+    C = Cn;
+    return true;
+}
+
 // W = A W A^T + Q (D x D, Smith doubling: W = sum_k A^k Q A^kT)
 MatL lyap_doubling(const MatL &A, const MatL &Q, int D) {
     MatL W = Q, Ak = A;
@@ -205,10 +316,10 @@ void cascade_df2t(const std::vector<double> &sos, int S, MatL &A, std::vector<LD
     d = step(e, 1.0L, B);
 }
 
-void put_dense(float *dst, const MatL &m, int D) {
+void put_dense(float *dst, const MatL &m, int D, bool dense) {
     const int DP = wpk::lb_dp(D);
     for (int r = 0; r < D; ++r)
-        for (int q = 0; q < DP; ++q) dst[r * DP + q] = (q < D && q < wpk::lt_nj(r)) ? (float)m[r * D + q] : 0.f;
+        for (int q = 0; q < DP; ++q) dst[r * DP + q] = (q < D && q < wpk::lt_nj(D, r, dense)) ? (float)m[r * D + q] : 0.f;
 }
 
 int exp_of(double v) {
@@ -219,7 +330,11 @@ int exp_of(double v) {
 
 template <int D, int NOP>
 cudaError_t set_attr(size_t smem) {
-    return cudaFuncSetAttribute(wpk::chain_lb_kernel<D, NOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(wpk::chain_lb_kernel<D, NOP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(wpk::chain_lb_kernel<D, NOP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
 }
 
 template <int D>
@@ -243,43 +358,21 @@ cudaError_t set_attr_any(int D, int nop, size_t smem) {
 
 }  // namespace
 
-size_t lb_smem_bytes(int D, int H, int nop, bool tma) {
-    return wpk::LbLayout(wpk::CT_TOUT + H, H + 64, D, nop, tma).total;
+size_t lb_smem_bytes(int D, int H, int nop, bool tma, bool dense) {
+    return wpk::LbLayout(wpk::CT_TOUT + H, H + 64, D, nop, tma, dense).total;
 }
 
-bool lb_fits(int S, int T) {
-    if (S < 1 || S > 8) return false;
-    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
-    if (H > wpk::LB_MAX_H) return false;
-    return lb_smem_bytes(2 * S, H, 2, false) <= 227 * 1024;
-}
-
-void lb_free(LbPlan &p) {
-    if (p.d_bimg) cudaFree(p.d_bimg);
-    if (p.d_stabs) cudaFree(p.d_stabs);
-    if (p.d_MTl) cudaFree(p.d_MTl);
-    p.d_bimg = nullptr;
-    p.d_stabs = p.d_MTl = nullptr;
-}
-
-int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps_in, double gain,
-             std::string &err) {
+// The per-section balanced, cascade-rescaled state basis of a cascade (block lower
+// triangular A): the basis every chain_lb plan starts from.
+void block_basis(const std::vector<double> &sos, int S, MatL &A, std::vector<LD> &B, std::vector<LD> &C, LD &d,
+                 int &balanced) {
     const int D = 2 * S;
-    const std::vector<double> f = taps_in.empty() ? std::vector<double>{1.0} : taps_in;
-    const int T = (int)f.size();
-    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
-    const int K = H + 64, W = wpk::CT_TOUT + H;
-    if (!lb_fits(S, T)) {
-        err = "chain pass does not fit the single-pass kernel";
-        return WP_EUNSUP;
-    }
     // ---- state space in the per-section balanced basis ----
     MatL A0;
     std::vector<LD> B0, C0;
-    LD d = 0;
     cascade_df2t(sos, S, A0, B0, C0, d);
     MatL Tm((size_t)D * D, 0.0L), Ti((size_t)D * D, 0.0L);
-    int balanced = 0;
+    balanced = 0;
     for (int s = 0; s < S; ++s) {
         LD t[4], ti[4];
         if (!balance_section(&sos[5 * s], t, ti)) {
@@ -294,8 +387,9 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
                 Ti[(2 * s + i) * D + 2 * s + j] = ti[i * 2 + j];
             }
     }
-    MatL A = mat_mul(mat_mul(Tm, A0, D), Ti, D);
-    std::vector<LD> B(D, 0.0L), C(D, 0.0L);
+    A = mat_mul(mat_mul(Tm, A0, D), Ti, D);
+    B.assign(D, 0.0L);
+    C.assign(D, 0.0L);
     for (int i = 0; i < D; ++i)
         for (int j = 0; j < D; ++j) {
             B[i] += Tm[i * D + j] * B0[j];
@@ -326,10 +420,94 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
             for (int j = 0; j < D; ++j) A[i * D + j] *= al[i] / al[j];
         }
     }
+}
+
+// fp32 roundoff gain of a basis: sqrt(sum_i Wc_ii Wo_ii) / sqrt(C Wc C^T)
+double basis_ratio(const MatL &A, const std::vector<LD> &B, const std::vector<LD> &C, int D) {
+    MatL Qc((size_t)D * D), Qo((size_t)D * D), At((size_t)D * D);
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            Qc[i * D + j] = B[i] * B[j];
+            Qo[i * D + j] = C[i] * C[j];
+            At[i * D + j] = A[j * D + i];
+        }
+    const MatL Wc = lyap_doubling(A, Qc, D), Wo = lyap_doubling(At, Qo, D);
+    LD noise = 0, sig = 0;
+    for (int i = 0; i < D; ++i) {
+        noise += Wc[i * D + i] * Wo[i * D + i];
+        for (int j = 0; j < D; ++j) sig += C[i] * Wc[i * D + j] * C[j];
+    }
+    return sig > 0 ? (double)std::sqrt(noise / sig) : 0.0;
+}
+
+// true when a cascade's block basis is ill-conditioned in fp32 (plan-time basis choice)
+bool lb_ill_conditioned(const double *sos, int S) {
+    if (S < 1 || S > 8) return false;
+    MatL A;
+    std::vector<LD> B, C;
+    LD d = 0;
+    int balanced = 0;
+    block_basis(std::vector<double>(sos, sos + 5 * S), S, A, B, C, d, balanced);
+    return basis_ratio(A, B, C, 2 * S) > kDenseRatio;
+}
+
+bool lb_fits(int S, int T) {
+    if (S < 1 || S > 8) return false;
+    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
+    if (H > wpk::LB_MAX_H) return false;
+    return lb_smem_bytes(2 * S, H, 2, false, false) <= 227 * 1024;
+}
+
+void lb_free(LbPlan &p) {
+    if (p.d_bimg) cudaFree(p.d_bimg);
+    if (p.d_stabs) cudaFree(p.d_stabs);
+    if (p.d_MTl) cudaFree(p.d_MTl);
+    p.d_bimg = nullptr;
+    p.d_stabs = p.d_MTl = nullptr;
+}
+
+int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector<double> &taps_in, double gain,
+             std::string &err) {
+    const int D = 2 * S;
+    const std::vector<double> f = taps_in.empty() ? std::vector<double>{1.0} : taps_in;
+    const int T = (int)f.size();
+    const int H = T > 1 ? (T - 1 + 15) / 16 * 16 : 0;
+    const int K = H + 64, W = wpk::CT_TOUT + H;
+    if (!lb_fits(S, T)) {
+        err = "chain pass does not fit the single-pass kernel";
+        return WP_EUNSUP;
+    }
+    MatL A;
+    std::vector<LD> B, C;
+    LD d = 0;
+    int balanced = 0;
+    block_basis(sos, S, A, B, C, d, balanced);
+    // fp32 conditioning of this block basis: roundoff in the states reaches the output
+    // with gain ~ sqrt(sum_i Wc_ii Wo_ii) against the signal's sqrt(C Wc C^T) (2.8 for
+    // cfg3, 4.8 cfg5; random 6-section cascades reach ~1700). Past kDenseRatio the
+    // plan switches to a globally balanced, dense basis where it fits
+    bool dense = false;
+    {
+        const double ratio = basis_ratio(A, B, C, D);
+        p.cond_ratio = ratio;
+        const char *fd = std::getenv("WP_LB_DENSE");  // 1 / 0 force (A/B, tests)
+        const bool want = fd ? std::atoi(fd) != 0 : ratio > kDenseRatio;
+        if (want && lb_smem_bytes(D, H, 2, false, true) <= 227 * 1024) {
+            MatL A2 = A;
+            std::vector<LD> B2 = B, C2 = C;
+            if (global_balance(A2, B2, C2, D)) {
+                A = A2;
+                B = B2;
+                C = C2;
+                dense = true;
+            }
+        }
+    }
+    p.dense = dense;
     // the transform keeps A block lower triangular; drop rounding residue above the blocks
     MatL Ac = A;
     for (int r = 0; r < D; ++r)
-        for (int q = wpk::lt_nj(r); q < D; ++q) Ac[r * D + q] = 0.0L;
+        for (int q = wpk::lt_nj(D, r, dense); q < D; ++q) Ac[r * D + q] = 0.0L;
     // ---- C A^t, impulse response, combined response g, state term E, e weights ----
     std::vector<LD> CA((size_t)(K + 1) * D);
     {
@@ -423,7 +601,7 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     }
     // ---- scan tables ----
     const MatL M = mat_pow(Ac, 64, D);
-    std::vector<float> st((size_t)wpk::lb_tab_floats(D), 0.f);
+    std::vector<float> st((size_t)wpk::lb_tab_floats(D, dense), 0.f);
     // E in pairs for the epilogue's packed FMAs: [q2][d2] = (E[2q2][2d2], E[2q2+1][2d2], E[2q2][2d2+1], E[2q2+1][2d2+1])
     for (int q2 = 0; q2 < 32; ++q2)
         for (int d2 = 0; d2 < D / 2; ++d2)
@@ -432,21 +610,21 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     {
         MatL m = M;
         for (int b = 0; b < 7; ++b) {
-            put_dense(&st[wpk::lb_off_mp(D) + b * D * wpk::lb_dp(D)], m, D);
+            put_dense(&st[wpk::lb_off_mp(D) + b * D * wpk::lb_dp(D)], m, D, dense);
             m = mat_mul(m, m, D);
         }
         const MatL M32 = mat_pow(M, 32, D);
         MatL w = mat_eye(D);
         for (int q = 0; q < 4; ++q) {
-            put_dense(&st[wpk::lb_off_wt(D) + q * D * wpk::lb_dp(D)], w, D);
+            put_dense(&st[wpk::lb_off_wt(D) + q * D * wpk::lb_dp(D)], w, D, dense);
             w = mat_mul(w, M32, D);
         }
         if (wpk::lb_has_gl(D)) {
             MatL gm = mat_eye(D);
             for (int l = 0; l < 32; ++l) {
                 for (int r = 0; r < D; ++r)
-                    for (int q = 0; q < wpk::lt_nj(r); ++q)
-                        st[wpk::lb_off_gl(D) + (size_t)(wpk::lt_off(r) + q) * 32 + l] = (float)gm[r * D + q];
+                    for (int q = 0; q < wpk::lt_nj(D, r, dense); ++q)
+                        st[wpk::lb_off_gl(D) + (size_t)(wpk::lt_off(D, r, dense) + q) * 32 + l] = (float)gm[r * D + q];
                 gm = mat_mul(gm, M, D);
             }
         }
@@ -485,9 +663,9 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     p.K = K;
     p.W = W;
     // TMA output staging where it fits next to two operand stages, three stages where they fit
-    p.tma_stage = LB_TMA_Y && lb_smem_bytes(D, H, 2, true) <= 227 * 1024;
-    p.nop = lb_smem_bytes(D, H, 3, p.tma_stage) <= 227 * 1024 ? 3 : 2;
-    p.smem = lb_smem_bytes(D, H, p.nop, p.tma_stage);
+    p.tma_stage = LB_TMA_Y && lb_smem_bytes(D, H, 2, true, dense) <= 227 * 1024;
+    p.nop = lb_smem_bytes(D, H, 3, p.tma_stage, dense) <= 227 * 1024 ? 3 : 2;
+    p.smem = lb_smem_bytes(D, H, p.nop, p.tma_stage, dense);
     // the attribute is per kernel, shared by every plan of this (D, stages) shape: set the maximum
     e = set_attr_any(D, p.nop, 227 * 1024);
     if (e != cudaSuccess) {
@@ -497,9 +675,9 @@ int lb_build(LbPlan &p, const std::vector<double> &sos, int S, const std::vector
     char buf[256];
     snprintf(buf, sizeof buf,
              "chain_lb[iir=%d fir=%d gain=%g] tcgen05 f16x3 M128xN%d K=%d halo=%d tile=%d stages=%d smem=%zu "
-             "fp32 scan (balanced basis, %d/%d sections), look-back, %s out",
-             S, T > 1 ? T : 0, gain, wpk::LB_NS, K, H, wpk::CT_TOUT, p.nop, p.smem, balanced, S,
-             p.tma_stage ? "TMA" : "LDS/STG");
+             "fp32 scan (%s basis, %d/%d sections), look-back, %s out",
+             S, T > 1 ? T : 0, gain, wpk::LB_NS, K, H, wpk::CT_TOUT, p.nop, p.smem,
+             dense ? "globally balanced dense" : "balanced", balanced, S, p.tma_stage ? "TMA" : "LDS/STG");
     p.desc = buf;
     return WP_OK;
 }
@@ -515,11 +693,16 @@ size_t lb_workspace_bytes(const LbPlan &p, long long C, long long tiles) { retur
 
 namespace {
 template <int D>
-cudaError_t launch_d(int nop, const wpk::LbArgs &a, const CUtensorMap &ymap, int grid, size_t smem, cudaStream_t st) {
-    if (nop == 3)
-        wpk::chain_lb_kernel<D, 3><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
+cudaError_t launch_d(int nop, bool dense, const wpk::LbArgs &a, const CUtensorMap &ymap, int grid, size_t smem,
+                     cudaStream_t st) {
+    if (nop == 3 && dense)
+        wpk::chain_lb_kernel<D, 3, true><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
+    else if (nop == 3)
+        wpk::chain_lb_kernel<D, 3, false><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
+    else if (dense)
+        wpk::chain_lb_kernel<D, 2, true><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
     else
-        wpk::chain_lb_kernel<D, 2><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
+        wpk::chain_lb_kernel<D, 2, false><<<grid, wpk::LB_THREADS, smem, st>>>(a, ymap);
     return cudaGetLastError();
 }
 
@@ -561,14 +744,14 @@ cudaError_t lb_launch(const LbPlan &p, const float *x, float *y, long long C, lo
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(tiles, sm_count());
     switch (p.D) {
-        case 2: e = launch_d<2>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 4: e = launch_d<4>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 6: e = launch_d<6>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 8: e = launch_d<8>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 10: e = launch_d<10>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 12: e = launch_d<12>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 14: e = launch_d<14>(p.nop, a, ymap, grid, p.smem, st); break;
-        case 16: e = launch_d<16>(p.nop, a, ymap, grid, p.smem, st); break;
+        case 2: e = launch_d<2>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 4: e = launch_d<4>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 6: e = launch_d<6>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 8: e = launch_d<8>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 10: e = launch_d<10>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 12: e = launch_d<12>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 14: e = launch_d<14>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
+        case 16: e = launch_d<16>(p.nop, p.dense, a, ymap, grid, p.smem, st); break;
         default: return cudaErrorInvalidValue;
     }
     count_launch();

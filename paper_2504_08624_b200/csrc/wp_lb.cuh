@@ -115,8 +115,8 @@ struct LbArgs {
 __host__ __device__ constexpr int lb_de(int D) { return D <= 8 ? 8 : 16; }
 __host__ __device__ constexpr int lb_dp(int D) { return (D + 3) & ~3; }
 __host__ __device__ constexpr int lb_has_gl(int D) { return D <= LB_GL_MAXD; }
-__host__ __device__ constexpr int lb_tab_floats(int D) {
-    return 64 * D + 11 * D * lb_dp(D) + (lb_has_gl(D) ? 32 * lt_size(D) : 0);
+__host__ __device__ constexpr int lb_tab_floats(int D, bool dense) {
+    return 64 * D + 11 * D * lb_dp(D) + (lb_has_gl(D) ? 32 * lt_size(D, dense) : 0);
 }
 __host__ __device__ constexpr int lb_off_mp(int D) { return 64 * D; }
 __host__ __device__ constexpr int lb_off_wt(int D) { return 64 * D + 7 * D * lb_dp(D); }
@@ -132,7 +132,7 @@ struct LbLayout {
     uint32_t total;
     // tma: 8 KB of staging per epilogue warp (two 32 x 32 TMA boxes) instead of 32 padded
     // half rows; chosen per plan only where it still fits (fusion reach is unchanged)
-    __host__ __device__ LbLayout(int W, int K, int D, int nop, bool tma) {
+    __host__ __device__ LbLayout(int W, int K, int D, int nop, bool tma, bool dense) {
         opBytes = ((uint32_t)W * 2u + 1023u) & ~1023u;
         bBytes = lb_bbytes(K);
         bimg = 0;
@@ -140,7 +140,7 @@ struct LbLayout {
         raw = op + 2u * (uint32_t)nop * opBytes;
         const uint32_t rawBytes = ((uint32_t)W * 4u + 1023u) & ~1023u;
         tabs = raw + rawBytes;
-        ring = (tabs + 4u * (uint32_t)lb_tab_floats(D) + 127u) & ~127u;  // [NL][D][128] row prefixes
+        ring = (tabs + 4u * (uint32_t)lb_tab_floats(D, dense) + 127u) & ~127u;  // [NL][D][128] row prefixes
         // [4 warps][32 rows] staging, 1024-aligned (TMA SWIZZLE_128B boxes: 2 x 4 KB per warp)
         stg = (ring + 4u * (uint32_t)(LB_NL * D * CT_ROWS) + 1023u) & ~1023u;
         misc = stg + (tma ? 4u * 8192u : 4u * 32u * CT_STG_PITCH);
@@ -201,15 +201,15 @@ __device__ __forceinline__ void wait_word(const unsigned long long *p) {
 }
 
 // out += M v for a block-lower-triangular M stored dense ([D][DP], 16-B
-// aligned rows): row r needs columns < lt_nj(r), read as float4
-template <int D>
+// aligned rows): row r needs columns < lt_nj(D, r, DN), read as float4
+template <int D, bool DN>
 __device__ __forceinline__ void lt_mv4(float (&out)[D], const float *m, const float (&v)[D]) {
     constexpr int DP = lb_dp(D);
 #pragma unroll
     for (int r = 0; r < D; ++r) {
         float acc = out[r];
 #pragma unroll
-        for (int q4 = 0; q4 < (lt_nj(r) + 3) / 4; ++q4) {
+        for (int q4 = 0; q4 < (lt_nj(D, r, DN) + 3) / 4; ++q4) {
             const float4 mm = *reinterpret_cast<const float4 *>(m + r * DP + 4 * q4);
             acc = fmaf(mm.x, v[4 * q4], acc);
             if (4 * q4 + 1 < D) acc = fmaf(mm.y, v[(4 * q4 + 1) % D], acc);
@@ -274,7 +274,7 @@ __device__ __forceinline__ void ffma2(float &a0, float &a1, float e0, float e1, 
 
 // s += M^lane V (M^l for l = lane < 32): lane-minor table Gl for D <= 8, else
 // five conditional squarings-table steps (Mp[b] = M^(2^b))
-template <int D>
+template <int D, bool DN>
 __device__ __forceinline__ void add_mlane(float (&s)[D], float (&V)[D], const float *Mp, const float *Gl, int lane) {
     constexpr int DP = lb_dp(D);
     if constexpr (lb_has_gl(D)) {
@@ -282,7 +282,7 @@ __device__ __forceinline__ void add_mlane(float (&s)[D], float (&V)[D], const fl
         for (int r = 0; r < D; ++r) {
             float acc = s[r];
 #pragma unroll
-            for (int q = 0; q < lt_nj(r); ++q) acc = fmaf(Gl[(lt_off(r) + q) * 32 + lane], V[q], acc);
+            for (int q = 0; q < lt_nj(D, r, DN); ++q) acc = fmaf(Gl[(lt_off(D, r, DN) + q) * 32 + lane], V[q], acc);
             s[r] = acc;
         }
     } else {
@@ -291,7 +291,7 @@ __device__ __forceinline__ void add_mlane(float (&s)[D], float (&V)[D], const fl
             float t[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) t[d] = 0.f;
-            lt_mv4<D>(t, Mp + b * D * DP, V);
+            lt_mv4<D, DN>(t, Mp + b * D * DP, V);
             if ((lane >> b) & 1) {
 #pragma unroll
                 for (int d = 0; d < D; ++d) V[d] = t[d];
@@ -338,7 +338,10 @@ __device__ __forceinline__ float reduce_scatter(const float (&w)[D], int lane, i
 
 }  // namespace lbd
 
-template <int D, int NOP>
+// DN: the plan's state basis is globally balanced (dense transfer matrices) instead of
+// per-section balanced (block lower triangular) - chosen at plan time for cascades
+// whose block basis is ill-conditioned in fp32
+template <int D, int NOP, bool DN>
 __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a, const __grid_constant__ CUtensorMap ymap) {
     static_assert(D >= 2 && D <= 16 && (D % 2) == 0, "2..8 sections");
     static_assert(NOP == 2 || NOP == 3, "two or three fp16 operand stages");
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
     unsigned char *smem = smem_raw + ((1024u - (wptc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nk = a.K / 16;
-    const LbLayout lay(a.W, a.K, D, NOP, a.tma_stage != 0);
+    const LbLayout lay(a.W, a.K, D, NOP, a.tma_stage != 0, DN);
     unsigned char *bimg = smem + lay.bimg;
     unsigned char *op = smem + lay.op;
     float *tabs = reinterpret_cast<float *>(smem + lay.tabs);
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
     }
     for (int i = tid; i < (int)(lay.bBytes / 16); i += LB_THREADS)
         reinterpret_cast<uint4 *>(bimg)[i] = reinterpret_cast<const uint4 *>(a.Bimg)[i];
-    for (int i = tid; i < lb_tab_floats(D); i += LB_THREADS) tabs[i] = a.stabs[i];
+    for (int i = tid; i < lb_tab_floats(D, DN); i += LB_THREADS) tabs[i] = a.stabs[i];
     if (tid < LB_RING) stag[tid] = -1;
     wptc::fence_proxy_async_smem();
     wptc::fence_before_sync();
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
                 float prev[D];
 #pragma unroll
                 for (int d = 0; d < D; ++d) prev[d] = __shfl_up_sync(0xffffffffu, P[d], off);
-                if (lane >= off) lbd::lt_mv4<D>(P, Mp + b * D * DP, prev);
+                if (lane >= off) lbd::lt_mv4<D, DN>(P, Mp + b * D * DP, prev);
             }
             // exclusive: state entering the row from the warp start (zero carry)
             float s[D];
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
                 float t[D];
 #pragma unroll
                 for (int d = 0; d < D; ++d) t[d] = Tg[u * D + d];
-                lbd::lt_mv4<D>(t, Mp + 5 * D * DP, V);
+                lbd::lt_mv4<D, DN>(t, Mp + 5 * D * DP, V);
 #pragma unroll
                 for (int d = 0; d < D; ++d) V[d] = t[d];
             }
@@ -677,12 +680,12 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
                 float agg[D];
 #pragma unroll
                 for (int d = 0; d < D; ++d) agg[d] = Tg[3 * D + d];
-                lbd::lt_mv4<D>(agg, Mp + 5 * D * DP, V);
+                lbd::lt_mv4<D, DN>(agg, Mp + 5 * D * DP, V);
 #pragma unroll
                 for (int d = 0; d < D; ++d) lbd::st_word(a.aggw + tile * D + d, agg[d]);
             }
             // L_m = s + M^lane Z_w: the state entering row m at zero carry from the tile start
-            lbd::add_mlane<D>(s, V, Mp, Gl, lane);
+            lbd::add_mlane<D, DN>(s, V, Mp, Gl, lane);
             if (row == 0) LBTR(tile, 12);
             // only now (the aggregate is out) wait for the ring slot
             wptc::mbar_wait_sleep<256>(LEM(sl), (uint32_t)((i / LB_NL) & 1) ^ 1u);
@@ -721,8 +724,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1) chain_lb_kernel(const LbArgs a,
 #pragma unroll
                 for (int d = 0; d < D; ++d) cin[d] = cb[sc4 * D + d], V[d] = 0.f;
                 ctd::arrive(CEM(sc4));
-                lbd::lt_mv4<D>(V, Wt + wq * D * DP, cin);
-                lbd::add_mlane<D>(s, V, Mp, Gl, lane);
+                lbd::lt_mv4<D, DN>(V, Wt + wq * D * DP, cin);
+                lbd::add_mlane<D, DN>(s, V, Mp, Gl, lane);
             }
             if (row == 0) LBTR(tile, 11);
             wptc::mbar_wait(EFL(sa), (uint32_t)((i / LB_NA) & 1));  // completed before the scan: ordering only

@@ -182,3 +182,23 @@ def test_multitile_random_chains():
         y, ref = _run(stages, x, fs)
         tol = FIR_TOL if kind == "fir_tc" else IIR_TOL
         assert oracle.parity_error(y, ref) <= tol, (case, kind, C, N, T)
+
+
+def test_ill_conditioned_random_cascade_dense_basis():
+    """The worst of 1500 random 6-section cascades (the reference's generator,
+    tools/six_section_probe.py seed 5, case 1407): its per-section balanced basis
+    has an fp32 roundoff gain of ~1700, so the plan keeps the run in one pass and
+    switches to the globally balanced (dense) basis - 1.4e-4 of the peak before,
+    under 1e-5 after."""
+    from conftest import random_stable_section
+
+    rng = np.random.default_rng(5)
+    for _ in range(1408):
+        f = wp.IirFilter.from_sections([random_stable_section(rng) for _ in range(6)], 44100,
+                                       overall_gain=float(rng.uniform(0.25, 2.0)))
+        C, N = int(rng.integers(1, 13)), int(10 ** rng.uniform(4, 5.5))
+        x = rng.standard_normal((C, N))
+    desc = engine.plan_for(wp.Chain([f]).bind(44100).stages, device=0).describe_for(C, N)
+    assert len(desc) == 1 and "globally balanced dense" in desc[0], desc
+    y, ref = _run([f], x, 44100)
+    assert oracle.parity_error(y, ref) <= 1e-5
