@@ -27,6 +27,7 @@ unpinned").
 from __future__ import annotations
 
 import cmath
+import functools
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence, Union
@@ -618,7 +619,12 @@ def design_fir(kind, num_taps: int, fc, window: str = "hamming", fs: Optional[in
 # ---------------------------------------------------------------------------
 
 
+@functools.lru_cache(maxsize=512)
 def _design_iir_from_spec(spec: FilterSpec, fs: int) -> IirFilter:
+    """Bind-time design, memoised per (spec, fs): a bound filter is immutable
+    (frozen sections), so every ``pipe`` of the same unbound chain at the same
+    rate reuses one design instead of re-running the zpk/bilinear maths on the
+    host (the reference re-designs on every bind, chain.py:56-64)."""
     fam = spec.family
     if fam == "butterworth":
         return design_butterworth(spec.kind, spec.order, spec.fc, fs)
@@ -631,7 +637,9 @@ def _design_iir_from_spec(spec: FilterSpec, fs: int) -> IirFilter:
     raise InvalidArgument(f"cannot bind IIR spec of family {fam!r}")
 
 
+@functools.lru_cache(maxsize=512)
 def _design_fir_from_spec(spec: FilterSpec, fs: int) -> FirFilter:
+    """Memoised like _design_iir_from_spec (taps are a read-only copy)."""
     if spec.family == "fir_sinc":
         return design_fir(spec.kind, spec.order, spec.fc, spec.window, fs)
     raise InvalidArgument(f"cannot bind FIR spec of family {spec.family!r}")

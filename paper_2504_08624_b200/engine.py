@@ -307,7 +307,7 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
         # (every other pass is per channel); ~16-32 blocks balance the
         # first-upload / last-download ramp against per-block launch overhead
         pairs = any(d.startswith("fft_ols") for d in plan.describe())
-        nblk = blocks or max(1, min((C + 1) // 2, 32))
+        nblk = blocks or max(1, min((C + 1) // 2 if pairs else C, 32))
         parts = [(a, b) for a, b in partition(C, nblk, align=2 if pairs else 1) if b > a]
         s_in, s_run, s_out = _copy_streams(dev)
         x = torch.empty((C, N), dtype=torch.float32, device=dev)

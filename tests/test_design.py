@@ -136,3 +136,21 @@ def test_gain_and_normalize_stages():
     with pytest.raises(wp.InvalidArgument):
         wp.Normalize(0.0)
     assert np.allclose(wp.frequency_response(wp.Gain(2.0, fs=FS), [0.0, 100.0]), 2.0)
+
+
+def test_bind_memoised_per_spec_and_rate():
+    """Binding an unbound design reuses one immutable design per (spec, fs)
+    (host-side cache; the coefficients equal a direct design)."""
+    import paper_2504_08624_b200 as wp
+
+    lp = wp.design_butterworth("lp", 4, 1000)
+    a, b = lp.bind(44100), lp.bind(44100)
+    assert a is b
+    direct = wp.design_butterworth("lp", 4, 1000, 44100)
+    assert np.array_equal(a.sos_rows(), direct.sos_rows())
+    assert lp.bind(48000) is not a
+    fir = wp.design_fir("lp", 101, 15000)
+    assert fir.bind(48000) is fir.bind(48000)
+    assert not fir.bind(48000).taps.flags.writeable
+    with pytest.raises(wp.SampleRateMismatch):
+        a.bind(48000)
