@@ -85,6 +85,21 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t chann
                     int64_t ld_x, int64_t ld_y, void *workspace, size_t workspace_bytes,
                     wp_stream_t stream);
 
+/* Host buffers in, host buffers out (the e2e path; Wave.numpy32 over a pinned
+ * source): channel blocks (single channels, or pairs when a pass runs the FFT
+ * path; `blocks` <= 0 = up to 32) are uploaded, executed and downloaded on
+ * three internal streams so both PCIe directions and the kernels overlap.
+ * dx, dy: distinct device buffers of [channels x frames] floats (row stride =
+ * frames); workspace: wp_plan_workspace_bytes of the largest block (the whole
+ * call's size always suffices). Asynchronous: `stream` waits for the last
+ * download, so synchronise it before reading hy. Pinned host buffers give the
+ * overlap; pageable ones still work. Not for chains with Normalize (the peak
+ * spans all blocks): WP_EUNSUP. Replaces the reference's host-side
+ * Chain.apply loop (chain.py:66-71) over numpy buffers for an FFI caller. */
+int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_t channels, int64_t frames,
+                         int64_t ld_hx, int64_t ld_hy, float *dx, float *dy, void *workspace,
+                         size_t workspace_bytes, int32_t blocks, wp_stream_t stream);
+
 /* Number of fused passes and of kernel launches per execute call. */
 int wp_plan_num_passes(const wp_plan *plan);
 int wp_plan_launches(const wp_plan *plan);

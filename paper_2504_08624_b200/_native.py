@@ -40,6 +40,7 @@ EXPORTED = (
     "wp_plan_destroy",
     "wp_plan_workspace_bytes",
     "wp_plan_execute",
+    "wp_plan_execute_host",
     "wp_plan_num_passes",
     "wp_plan_launches",
     "wp_plan_describe",
@@ -95,6 +96,7 @@ def load(require_device: bool = False):
             lib.wp_plan_destroy.argtypes = [vp]
             lib.wp_plan_workspace_bytes.argtypes = [vp, i64, i64, ctypes.POINTER(sz)]
             lib.wp_plan_execute.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, sz, vp]
+            lib.wp_plan_execute_host.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp, vp, vp, sz, i32, vp]
             lib.wp_plan_num_passes.argtypes = [vp]
             lib.wp_plan_launches.argtypes = [vp]
             lib.wp_plan_describe.argtypes = [vp, i32]
@@ -114,7 +116,7 @@ def load(require_device: bool = False):
             lib.wp_wav_decode.argtypes = [vp, i32, vp, i64, i64, i64, vp]
             lib.wp_wav_encode.argtypes = [vp, i64, i64, i64, i32, vp, vp, vp]
             for name in ("wp_plan_create", "wp_plan_destroy", "wp_plan_workspace_bytes", "wp_plan_execute",
-                         "wp_plan_num_passes", "wp_plan_launches", "wp_plan_launches_for", "wp_iir_cascade", "wp_fir",
+                         "wp_plan_execute_host", "wp_plan_num_passes", "wp_plan_launches", "wp_plan_launches_for", "wp_iir_cascade", "wp_fir",
                          "wp_iir_cascade_workspace", "wp_fir_workspace",
                          "wp_white_noise", "wp_peak_abs", "wp_abi_version", "wp_check_device", "wp_set_trace",
                          "wp_wav_decode", "wp_wav_encode"):
@@ -229,6 +231,15 @@ class Plan:
         check(
             self._lib.wp_plan_execute(self.handle, x_ptr, y_ptr, channels, frames, ldx, ldy, ws_ptr, ws_bytes, stream),
             "wp_plan_execute",
+        )
+
+    def execute_host(self, hx_ptr: int, hy_ptr: int, channels: int, frames: int, ld_hx: int, ld_hy: int,
+                     dx_ptr: int, dy_ptr: int, ws_ptr: int, ws_bytes: int, blocks: int, stream: int) -> None:
+        """Host in -> host out in overlapped channel blocks (wp_plan_execute_host)."""
+        check(
+            self._lib.wp_plan_execute_host(self.handle, hx_ptr, hy_ptr, channels, frames, ld_hx, ld_hy,
+                                           dx_ptr, dy_ptr, ws_ptr, ws_bytes, blocks, stream),
+            "wp_plan_execute_host",
         )
 
 

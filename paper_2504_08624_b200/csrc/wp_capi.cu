@@ -1015,6 +1015,111 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t C, in
     return WP_OK;
 }
 
+// ---- host -> device -> host streaming (the e2e path of Wave.numpy32) ----
+// Per device: an upload, a run and a download stream plus an event ring. One
+// mutex per process serialises the ENQUEUE of concurrent calls (the work
+// itself runs asynchronously), so an event is never re-recorded between a
+// call's record and the wait that consumes it.
+namespace {
+constexpr int kHostMaxBlocks = 32;
+struct HostStreams {
+    cudaStream_t in = nullptr, run = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr, ev_in[kHostMaxBlocks] = {}, ev_run[kHostMaxBlocks] = {}, done = nullptr;
+};
+std::mutex g_host_mu;
+std::map<int, HostStreams> g_host;
+
+int host_streams(int dev, HostStreams **out) {
+    auto it = g_host.find(dev);
+    if (it != g_host.end()) {
+        *out = &it->second;
+        return WP_OK;
+    }
+    HostStreams h;
+    cudaError_t e = cudaStreamCreateWithFlags(&h.in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h.run, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h.out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming);
+    for (int i = 0; i < kHostMaxBlocks && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&h.ev_in[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_run[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "stream/event creation");
+    *out = &(g_host[dev] = h);
+    return WP_OK;
+}
+}  // namespace
+
+int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_t C, int64_t N, int64_t ld_hx,
+                         int64_t ld_hy, float *dx, float *dy, void *workspace, size_t workspace_bytes,
+                         int32_t blocks, wp_stream_t stream_) {
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+    if (!plan) return fail(WP_EINVAL, "plan is NULL");
+    if (!hx || !hy || !dx || !dy) return fail(WP_EINVAL, "host and device buffers must be non-NULL");
+    if (C < 1 || N < 1) return fail(WP_EINVAL, "need channels >= 1 and frames >= 1");
+    if (ld_hx < N || ld_hy < N) return fail(WP_EINVAL, "row stride smaller than frames");
+    if (dx == dy) return fail(WP_EINVAL, "dx and dy must be distinct [C x N] device buffers");
+    bool pairs = false;  // the FFT path filters channel pairs together: pair-aligned blocks
+    for (const Pass &p : plan->passes) pairs = pairs || (p.kind != Pass::NORMALIZE && p.fft);
+    for (const Pass &p : plan->passes)
+        if (p.kind == Pass::NORMALIZE)
+            return fail(WP_EUNSUP, "a chain with Normalize needs the whole signal's peak: run wp_plan_execute");
+    const int64_t units = pairs ? (C + 1) / 2 : C;
+    int64_t nb = blocks > 0 ? blocks : kHostMaxBlocks;
+    nb = std::max<int64_t>(1, std::min<int64_t>({nb, units, (int64_t)kHostMaxBlocks}));
+    // contiguous blocks of units (as sharding.partition: the first r blocks one unit larger)
+    int64_t bounds[kHostMaxBlocks + 1];
+    size_t need = 0;
+    for (int64_t b = 0, a = 0; b <= nb; ++b) {
+        const int64_t u = b * (units / nb) + std::min<int64_t>(b, units % nb);
+        bounds[b] = std::min<int64_t>(C, pairs ? 2 * u : u);
+        if (b > 0) {
+            size_t r_off, t_off, w;
+            int64_t ld;
+            w = ws_layout(plan, bounds[b] - a, N, &r_off, &t_off, &ld);
+            need = std::max(need, w);
+        }
+        a = bounds[b];
+    }
+    if (!workspace || workspace_bytes < need)
+        return fail(WP_ENOMEM, "workspace too small: need " + std::to_string(need) + " bytes");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != plan->device) return fail(WP_EINVAL, "plan was created on another device");
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    HostStreams *h = nullptr;
+    if (int rc = host_streams(dev, &h)) return rc;
+    cudaError_t e = cudaEventRecord(h->start, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->in, h->start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->run, h->start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->start, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
+    const size_t row = sizeof(float) * (size_t)N;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t a = bounds[b], c = bounds[b + 1] - bounds[b];
+        if (c <= 0) continue;
+        e = cudaMemcpy2DAsync(dx + a * N, row, hx + a * ld_hx, sizeof(float) * ld_hx, row, c,
+                              cudaMemcpyHostToDevice, h->in);
+        if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[b], h->in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->run, h->ev_in[b], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "upload");
+        if (int rc = wp_plan_execute(plan, dx + a * N, dy + a * N, c, N, N, N, workspace, workspace_bytes,
+                                     reinterpret_cast<wp_stream_t>(h->run)))
+            return rc;
+        e = cudaEventRecord(h->ev_run[b], h->run);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->ev_run[b], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(hy + a * ld_hy, sizeof(float) * ld_hy, dy + a * N, row, row, c,
+                                  cudaMemcpyDeviceToHost, h->out);
+        if (e != cudaSuccess) return cuda_fail(e, "download");
+    }
+    e = cudaEventRecord(h->done, h->out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, h->done, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
+    return WP_OK;
+}
+
 // ---- seam-level one-shot entry points with a small plan cache ----
 // Plans are shared (std::shared_ptr): a caller holds its reference for the
 // duration of the execute call, so evicting an entry never frees a plan that

@@ -253,19 +253,6 @@ def execute_entries(entries, src, out=None):
     return out
 
 
-_streams = {}
-
-
-def _copy_streams(device):
-    import torch
-
-    key = device.index
-    if key not in _streams:
-        with torch.cuda.device(device):
-            _streams[key] = (torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device))
-    return _streams[key]
-
-
 def has_normalize(entries) -> bool:
     """A Normalize stage needs the peak of the WHOLE wave (design.Normalize), so
     such a chain cannot run block by block."""
@@ -294,7 +281,6 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     import torch
 
     from ._native import _require_cuda
-    from .sharding import partition
 
     _require_cuda()
     if has_normalize(entries):
@@ -303,37 +289,17 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):
         plan = _plans.get(dev.index, entries)
-        # the FFT path filters channel pairs together: keep its blocks pair-aligned
-        # (every other pass is per channel); ~16-32 blocks balance the
-        # first-upload / last-download ramp against per-block launch overhead
-        pairs = any(d.startswith("fft_ols") for d in plan.describe())
-        nblk = blocks or max(1, min((C + 1) // 2 if pairs else C, 32))
-        parts = [(a, b) for a, b in partition(C, nblk, align=2 if pairs else 1) if b > a]
-        s_in, s_run, s_out = _copy_streams(dev)
+        # the block loop (partition, three streams, events) runs in the native
+        # library: wp_plan_execute_host cuts single-channel blocks (pairs when
+        # a pass runs the FFT path), at most 32, and overlaps block b's upload,
+        # block b-1's pass and block b-2's download
         x = torch.empty((C, N), dtype=torch.float32, device=dev)
         y = torch.empty_like(x)
-        ws = _workspace(dev, s_run.cuda_stream, max(plan.workspace_bytes(b - a, N) for a, b in parts))
         cur = torch.cuda.current_stream(dev)
-        s_in.wait_stream(cur)
-        for a, b in parts:
-            with torch.cuda.stream(s_in):
-                x[a:b].copy_(host_src[a:b], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_in)
-            s_run.wait_event(ev_in)
-            plan.execute(x[a:b].data_ptr(), y[a:b].data_ptr(), b - a, N, N, N, ws.data_ptr(), ws.numel(),
-                         s_run.cuda_stream)
-            ev_run = torch.cuda.Event()
-            ev_run.record(s_run)
-            s_out.wait_event(ev_run)
-            with torch.cuda.stream(s_out):
-                host_out[a:b].copy_(y[a:b], non_blocking=True)
-        # keep the device buffers alive until the streams are done with them
-        x.record_stream(s_in)
-        x.record_stream(s_run)
-        y.record_stream(s_run)
-        y.record_stream(s_out)
-        s_out.synchronize()
+        ws = _workspace(dev, cur.cuda_stream, plan.workspace_bytes(C, N))
+        plan.execute_host(host_src.data_ptr(), host_out.data_ptr(), C, N, host_src.stride(0), host_out.stride(0),
+                          x.data_ptr(), y.data_ptr(), ws.data_ptr(), ws.numel(), int(blocks), cur.cuda_stream)
+        cur.synchronize()
     return host_out
 
 

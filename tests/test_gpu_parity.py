@@ -370,6 +370,50 @@ def test_streamed_host_path_bit_exact(C, fir_taps):
     assert np.array_equal((src | chain).numpy32(), ref)  # pinned result allocated internally
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("C", [1, 7])
+@pytest.mark.parametrize("blocks", [0, 1, 3, 64])
+@pytest.mark.parametrize("fft", [False, True])
+def test_plan_execute_host_blocks_strides(C, blocks, fft):
+    """wp_plan_execute_host (pinned and pageable host buffers, padded host row
+    strides, any block count, pair-aligned blocks on the FFT path) is
+    bit-identical to one device-resident wp_plan_execute; Normalize is refused."""
+    import torch
+
+    from paper_2504_08624_b200 import _native, engine
+
+    fs, N, ld = 48000, 20001, 20011
+    w = wp.white_noise(N / fs, C, fs, seed=5)
+    stages = [wp.design_fir("lp", 1500, 4000)] if fft else \
+        [wp.design_butterworth("hp", 4, 100), wp.design_fir("lp", 101, 4000), wp.Gain(0.5)]
+    chain = wp.Chain(stages)
+    ref = (w | chain).numpy32().copy()
+    bound = chain.bind(fs).stages
+    plan = engine.plan_for(bound)
+    assert any(d.startswith("fft_ols") for d in plan.describe()) == fft
+    for pin in (True, False):
+        hx = torch.full((C, ld), float("nan"), dtype=torch.float32, pin_memory=pin)
+        hx[:, :N].copy_(w.tensor())
+        hy = torch.full((C, ld), 7.0, dtype=torch.float32, pin_memory=pin)
+        dx = torch.empty((C, N), dtype=torch.float32, device="cuda")
+        dy = torch.empty_like(dx)
+        ws = torch.empty(plan.workspace_bytes(C, N), dtype=torch.uint8, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        plan.execute_host(hx.data_ptr(), hy.data_ptr(), C, N, ld, ld, dx.data_ptr(), dy.data_ptr(),
+                          ws.data_ptr(), ws.numel(), blocks, stream)
+        torch.cuda.current_stream().synchronize()
+        assert np.array_equal(hy[:, :N].numpy(), ref)
+        assert np.all(hy[:, N:].numpy() == 7.0)  # padding untouched
+    with pytest.raises(wp.WavepipeError):
+        plan.execute_host(hx.data_ptr(), hy.data_ptr(), C, N, ld, ld, dx.data_ptr(), dx.data_ptr(),
+                          ws.data_ptr(), ws.numel(), blocks, stream)  # dx == dy
+    norm = engine.plan_for(list(bound) + [wp.Normalize()])
+    with pytest.raises(wp.WavepipeError, match="Normalize"):
+        norm.execute_host(hx.data_ptr(), hy.data_ptr(), C, N, ld, ld, dx.data_ptr(), dy.data_ptr(),
+                          ws.data_ptr(), ws.numel(), blocks, stream)
+    assert _native.EXPORTED.count("wp_plan_execute_host") == 1
+
+
 # ---- FFT overlap-save path: ragged lengths, odd channel counts ---------------
 
 
