@@ -490,7 +490,7 @@ def main():
                      "kernel": " + ".join(kernels) + f" ({plan.launches_for(max(C, 1), N)} launch(es) per step)"},
         "e2e": {"value": total_units / e2e_s, "unit": "ch-samples/s", "h2d_bytes_per_step": units * 4,
                 "d2h_bytes_per_step": units * 4, "seconds_per_step": e2e_s,
-                "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned)"},
+                "path": "Wave.from_tensor(pinned) | Chain -> numpy32(out=pinned) = C-ABI wp_plan_execute_host on host buffers"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
