@@ -268,7 +268,7 @@ def normalize_scale(peak: float, target: float):
     return float(np.float32(target) / p)
 
 
-def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 0):
+def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 0, sync: bool = True):
     """Host -> device -> host execution of a recorded chain, overlapped.
 
     ``host_src`` and ``host_out`` are pinned float32 CPU tensors ``[C, N]``.
@@ -277,6 +277,9 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
     one launch over all channels); block b's upload, the fused pass over block
     b-1 and block b-2's download run concurrently on three streams, so the
     PCIe link carries both directions at once instead of one after the other.
+    ``sync=False`` returns once the work is enqueued (the device's current
+    stream waits for the last download; the device buffers go back to the
+    caching allocator on that stream, so reuse is ordered after it).
     """
     import torch
 
@@ -299,7 +302,8 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
         ws = _workspace(dev, cur.cuda_stream, plan.workspace_bytes(C, N))
         plan.execute_host(host_src.data_ptr(), host_out.data_ptr(), C, N, host_src.stride(0), host_out.stride(0),
                           x.data_ptr(), y.data_ptr(), ws.data_ptr(), ws.numel(), int(blocks), cur.cuda_stream)
-        cur.synchronize()
+        if sync:
+            cur.synchronize()
     return host_out
 
 

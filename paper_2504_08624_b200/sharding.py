@@ -107,6 +107,26 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
     if src is None:
         host_src = wave._pinned if getattr(wave, "_pinned", None) is not None else torch.from_numpy(
             np.ascontiguousarray(wave.numpy32()))
+    if host_src is not None and gather == "host" and host_src.is_pinned():
+        lazy = Wave.from_tensor(host_src, wave.fs) | chain
+        if lazy._host_streamable():
+            # pinned host in -> pinned host out: every device streams its block
+            # through wp_plan_execute_host (uploads, passes and downloads
+            # overlapped per device, all devices at once)
+            from .engine import stream_host_entries
+
+            if out is None:
+                out = torch.empty((C, N), dtype=torch.float32, pin_memory=C * N * 4 <= _PIN_MAX_BYTES)
+            _check_out(out, C, N)
+            if out.is_pinned():
+                used = []
+                for dev, (c0, c1) in zip(devs, blocks):
+                    if c1 > c0:
+                        stream_host_entries(lazy._entries, host_src[c0:c1], out[c0:c1], device=dev, sync=False)
+                        used.append(dev)
+                for dev in used:
+                    torch.cuda.synchronize(dev)
+                return Wave.from_tensor(out, wave.fs)
     shards = []
     for dev, (c0, c1) in zip(devs, blocks):
         if c1 == c0:
@@ -119,9 +139,7 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
         return [w for _, _, w in shards]
     if out is None:
         out = torch.empty((C, N), dtype=torch.float32, pin_memory=C * N * 4 <= _PIN_MAX_BYTES)
-    elif (not isinstance(out, torch.Tensor) or out.device.type != "cpu" or out.dtype != torch.float32
-          or tuple(out.shape) != (C, N)):
-        raise InvalidArgument(f"out must be a CPU float32 tensor of shape {(C, N)}")
+    _check_out(out, C, N)
     pinned = out.is_pinned()
     for (c0, c1), dev, w in shards:
         with torch.cuda.device(dev):
@@ -129,6 +147,13 @@ def shard_pipe(wave: Wave, stages, devices: Optional[Sequence] = None, gather: s
     for _, dev, _ in shards:
         torch.cuda.synchronize(dev)
     return Wave.from_tensor(out, wave.fs)
+
+
+def _check_out(out, C, N):
+    torch = _torch()
+    if (not isinstance(out, torch.Tensor) or out.device.type != "cpu" or out.dtype != torch.float32
+            or tuple(out.shape) != (C, N)):
+        raise InvalidArgument(f"out must be a CPU float32 tensor of shape {(C, N)}")
 
 
 def _run_segments(shards, chain, combine_peaks):

@@ -150,6 +150,30 @@ def test_pinned_source_chain_with_normalize_is_not_streamed_per_block():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fft", [False, True])
+def test_shard_pipe_pinned_source_streams_per_device(fft):
+    """A pinned host source is streamed per device through wp_plan_execute_host
+    (all devices enqueued, then synchronised), bit-identical to one device;
+    a pageable caller buffer takes the upload/run/gather path."""
+    import torch
+
+    fs = 48000
+    w = wp.white_noise(0.5, 7, fs, seed=13)
+    chain = wp.Chain([wp.design_fir("lp", 2048, 2000)]) if fft else \
+        wp.Chain([wp.design_butterworth("hp", 4, 100), wp.design_fir("lp", 101, 15000), wp.Gain(0.5)])
+    ref = (w | chain).samples
+    pinned = torch.empty((7, w.frames), dtype=torch.float32, pin_memory=True)
+    pinned.copy_(w.tensor())
+    src = wp.Wave.from_tensor(pinned, fs)
+    for devices in (None, [0, 0], [0, 0, 0]):
+        got = wp.shard_pipe(src, chain, devices=devices)
+        assert got._pinned is not None and got._pinned.is_pinned()
+        assert np.array_equal(got.samples, ref), devices
+    out = torch.empty((7, w.frames), dtype=torch.float32)
+    assert np.array_equal(wp.shard_pipe(src, chain, devices=[0, 0], out=out).samples, ref)
+
+
+@pytest.mark.gpu
 def test_shard_pipe_into_caller_buffer():
     """gather into a caller-provided host tensor (pinned or pageable), as a
     59 GB cfg5 output should be, instead of a fresh page-locked buffer."""
