@@ -1096,28 +1096,38 @@ int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_
     if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->start, 0);
     if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
     const size_t row = sizeof(float) * (size_t)N;
-    for (int64_t b = 0; b < nb; ++b) {
+    int rc = WP_OK;
+    for (int64_t b = 0; b < nb && rc == WP_OK; ++b) {
         const int64_t a = bounds[b], c = bounds[b + 1] - bounds[b];
         if (c <= 0) continue;
         e = cudaMemcpy2DAsync(dx + a * N, row, hx + a * ld_hx, sizeof(float) * ld_hx, row, c,
                               cudaMemcpyHostToDevice, h->in);
         if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[b], h->in);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(h->run, h->ev_in[b], 0);
-        if (e != cudaSuccess) return cuda_fail(e, "upload");
-        if (int rc = wp_plan_execute(plan, dx + a * N, dy + a * N, c, N, N, N, workspace, workspace_bytes,
-                                     reinterpret_cast<wp_stream_t>(h->run)))
-            return rc;
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "upload");
+            break;
+        }
+        rc = wp_plan_execute(plan, dx + a * N, dy + a * N, c, N, N, N, workspace, workspace_bytes,
+                             reinterpret_cast<wp_stream_t>(h->run));
+        if (rc != WP_OK) break;
         e = cudaEventRecord(h->ev_run[b], h->run);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->ev_run[b], 0);
         if (e == cudaSuccess)
             e = cudaMemcpy2DAsync(hy + a * ld_hy, sizeof(float) * ld_hy, dy + a * N, row, row, c,
                                   cudaMemcpyDeviceToHost, h->out);
-        if (e != cudaSuccess) return cuda_fail(e, "download");
+        if (e != cudaSuccess) rc = cuda_fail(e, "download");
     }
-    e = cudaEventRecord(h->done, h->out);
+    // even after an error, the caller's stream waits for everything already
+    // enqueued on the three streams (its buffers must outlive that work)
+    e = cudaEventRecord(h->ev_in[0], h->in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->ev_in[0], 0);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_run[0], h->run);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, h->ev_run[0], 0);
+    if (e == cudaSuccess) e = cudaEventRecord(h->done, h->out);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, h->done, 0);
-    if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
-    return WP_OK;
+    if (e != cudaSuccess && rc == WP_OK) rc = cuda_fail(e, "stream ordering");
+    return rc;
 }
 
 // ---- seam-level one-shot entry points with a small plan cache ----
