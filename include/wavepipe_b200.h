@@ -93,7 +93,9 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t chann
  * frames); workspace: wp_plan_workspace_bytes of the largest block (the whole
  * call's size always suffices). Asynchronous: `stream` waits for the last
  * download, so synchronise it before reading hy. Pinned host buffers give the
- * overlap; pageable ones still work. Not for chains with Normalize (the peak
+ * overlap; pageable ones still work. Every block runs the kernels the whole
+ * call's shape selects, so hy is bit-identical to one wp_plan_execute over all
+ * channels. Not for chains with Normalize (the peak
  * spans all blocks): WP_EUNSUP. Replaces the reference's host-side
  * Chain.apply loop (chain.py:66-71) over numpy buffers for an FFI caller. */
 int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_t channels, int64_t frames,

@@ -567,8 +567,13 @@ size_t rec_bytes(const Pass &p) {
 
 long long tiles_per_channel(const Pass &p, long long N) { return (N + p.Lout - 1) / p.Lout; }
 
+// wp_plan_execute_host runs channel blocks of one call: while it does, every
+// block takes the kernel route of the WHOLE call (t_route_C = its channels),
+// so the result is bit-identical to one wp_plan_execute over all channels
+static thread_local long long t_route_C = 0;
 bool uses_lb(const Pass &p, long long C, long long N) {
-    return p.lb || (p.lb_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * C >= p.lb_min_tiles);
+    const long long Cr = std::max(C, t_route_C);
+    return p.lb || (p.lb_large && ((N + wpk::CT_TOUT - 1) / wpk::CT_TOUT) * Cr >= p.lb_min_tiles);
 }
 
 // look-back records / scan buffers of one pass for a [C x N] call
@@ -1065,6 +1070,10 @@ int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_
     for (const Pass &p : plan->passes)
         if (p.kind == Pass::NORMALIZE)
             return fail(WP_EUNSUP, "a chain with Normalize needs the whole signal's peak: run wp_plan_execute");
+    struct RouteGuard {
+        explicit RouteGuard(long long c) { t_route_C = c; }
+        ~RouteGuard() { t_route_C = 0; }
+    } route(C);
     const int64_t units = pairs ? (C + 1) / 2 : C;
     int64_t nb = blocks > 0 ? blocks : kHostMaxBlocks;
     nb = std::max<int64_t>(1, std::min<int64_t>({nb, units, (int64_t)kHostMaxBlocks}));

@@ -8,9 +8,11 @@ The reference picks its kernel module in one place,
 
 This module has the same functions as ``_kernels_jit`` / ``_kernels_py``
 (``_kernels_jit.py:35-100``, ``_kernels_py.py:13-63``) -- float64 numpy in,
-new float64 numpy array out -- backed by the one-shot entry points of the C
-ABI (``wp_iir_cascade`` / ``wp_fir``, include/wavepipe_b200.h), with the
-device workspace sized per call by ``wp_*_workspace``. INTEGRATION.md shows
+new float64 numpy array out -- backed by the C ABI: calls up to 2 GiB of float32 run through
+``wp_plan_execute_host`` from page-locked staging (uploads, passes and
+downloads of channel blocks overlapped), larger ones through the one-shot
+entry points (``wp_iir_cascade`` / ``wp_fir``, include/wavepipe_b200.h) with
+the device workspace sized per call by ``wp_*_workspace``. INTEGRATION.md shows
 the two-line change that makes ``engine._kernels()`` return it. It is the
 seam for code that keeps the reference's per-stage engine; the lazy ``Wave``
 / ``Chain`` of this package fuses whole chains instead.
@@ -40,6 +42,7 @@ __all__ = [
 ]
 
 _dp = ctypes.POINTER(ctypes.c_double)
+_PIN_MAX_BYTES = 2 << 30  # larger calls copy through pageable memory (no page-locking of huge buffers)
 
 
 def _planar(x) -> np.ndarray:
@@ -62,6 +65,21 @@ def _run(kind: str, coef: np.ndarray, n: int, x: np.ndarray, flags: int) -> np.n
     need = ctypes.c_size_t()
     query = lib.wp_iir_cascade_workspace if kind == "iir" else lib.wp_fir_workspace
     _native.check(query(cp, n, C, N, flags, ctypes.byref(need)), f"{kind} workspace")
+    if C * N * 4 <= _PIN_MAX_BYTES:
+        # page-locked staging (the caching host allocator reuses it): the
+        # float64 -> float32 rounding writes straight into it, and
+        # wp_plan_execute_host overlaps uploads, passes and downloads of
+        # channel blocks (same plan and kernels as the one-shot entry below)
+        from . import engine
+
+        kind_id = _native.WP_STAGE_IIR if kind == "iir" else _native.WP_STAGE_FIR
+        c_ro = c.copy()
+        c_ro.setflags(write=False)
+        hx = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
+        np.copyto(hx.numpy(), x, casting="same_kind")
+        hy = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
+        engine.stream_host_entries(((kind_id, c_ro, 0.0, int(flags)),), hx, hy)
+        return hy.numpy().astype(np.float64)
     x32 = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
     y32 = torch.empty_like(x32)
     ws = torch.empty(max(int(need.value), 1), dtype=torch.uint8, device=x32.device)

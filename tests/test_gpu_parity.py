@@ -414,6 +414,28 @@ def test_plan_execute_host_blocks_strides(C, blocks, fft):
     assert _native.EXPORTED.count("wp_plan_execute_host") == 1
 
 
+@pytest.mark.gpu
+def test_plan_execute_host_blocks_take_the_whole_call_route():
+    """cfg1's shape (2 x 441000, LP4): the whole call runs chain_lb (108 tiles),
+    a one-channel block alone would take the CUDA-core scan (54 tiles); the
+    streamed blocks keep the whole call's route, so the e2e output is
+    bit-identical to the device-resident pass."""
+    import torch
+
+    fs = 44100
+    w = wp.white_noise(10.0, 2, fs, seed=42)
+    chain = wp.Chain([wp.design_butterworth("lp", 4, 1000)])
+    plan = __import__("paper_2504_08624_b200.engine", fromlist=["plan_for"]).plan_for(chain.bind(fs).stages)
+    assert plan.describe_for(2, w.frames)[0].startswith("chain_lb")
+    assert not plan.describe_for(1, w.frames)[0].startswith("chain_lb")
+    ref = (w | chain).numpy32().copy()
+    pinned = torch.empty((2, w.frames), dtype=torch.float32, pin_memory=True)
+    pinned.copy_(w.tensor())
+    out = torch.empty_like(pinned).pin_memory()
+    (wp.Wave.from_tensor(pinned, fs) | chain).numpy32(out=out)
+    assert np.array_equal(out.numpy(), ref)
+
+
 # ---- FFT overlap-save path: ragged lengths, odd channel counts ---------------
 
 
