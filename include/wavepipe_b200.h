@@ -87,7 +87,7 @@ int wp_plan_execute(const wp_plan *plan, const float *x, float *y, int64_t chann
 
 /* Host buffers in, host buffers out (the e2e path; Wave.numpy32 over a pinned
  * source): channel blocks (single channels, or pairs when a pass runs the FFT
- * path; `blocks` <= 0 = up to 32) are uploaded, executed and downloaded on
+ * path; `blocks` <= 0 = 16, or 32 from 4 GiB; at most 32) are uploaded, executed and downloaded on
  * three internal streams so both PCIe directions and the kernels overlap.
  * dx, dy: distinct device buffers of [channels x frames] floats (row stride =
  * frames); workspace: wp_plan_workspace_bytes of the largest block (the whole

@@ -1075,7 +1075,10 @@ int wp_plan_execute_host(const wp_plan *plan, const float *hx, float *hy, int64_
         ~RouteGuard() { t_route_C = 0; }
     } route(C);
     const int64_t units = pairs ? (C + 1) / 2 : C;
-    int64_t nb = blocks > 0 ? blocks : kHostMaxBlocks;
+    // default: 16 blocks (same-box probes: cfg3's 737 MB 2-3 % faster than 32:
+    // per-block copy/launch overhead), 32 from 4 GiB on (shorter ramp)
+    const int64_t dflt = (int64_t)sizeof(float) * C * N >= (4LL << 30) ? kHostMaxBlocks : 16;
+    int64_t nb = blocks > 0 ? blocks : dflt;
     nb = std::max<int64_t>(1, std::min<int64_t>({nb, units, (int64_t)kHostMaxBlocks}));
     // contiguous blocks of units (as sharding.partition: the first r blocks one unit larger)
     int64_t bounds[kHostMaxBlocks + 1];

@@ -294,7 +294,7 @@ def stream_host_entries(entries, host_src, host_out, device=None, blocks: int = 
         plan = _plans.get(dev.index, entries)
         # the block loop (partition, three streams, events) runs in the native
         # library: wp_plan_execute_host cuts single-channel blocks (pairs when
-        # a pass runs the FFT path), at most 32, and overlaps block b's upload,
+        # a pass runs the FFT path), 16 (32 from 4 GiB), and overlaps block b's upload,
         # block b-1's pass and block b-2's download
         x = torch.empty((C, N), dtype=torch.float32, device=dev)
         y = torch.empty_like(x)
